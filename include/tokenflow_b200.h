@@ -1,0 +1,243 @@
+/*
+ * tokenflow_b200.h - C ABI of the B200-native TokenFlow KV-movement hot path.
+ *
+ * One shared library (paper_2510_02758_b200/_tf_b200.so, sm_100a) exporting
+ * plain-C entry points: raw pointers, sizes, cudaStream_t passed as void*.
+ * No torch types cross this boundary; the Python host (ctypes) and any other
+ * FFI bind it directly (INTEGRATION.md shows the bindings).
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src):
+ *   tf_pool_* / tf_blocks_* / tf_table_apply
+ *       token-denominated ledger + KvResidency      tokensim/engine.py:325-365,
+ *                                                    tokensim/kvstore.py:35-59
+ *   tf_kv_gather_d2h   writethrough + evict chunks  tokensim/engine.py:781-813, :843-848
+ *                      transfer_time (d2h)          tokensim/costs.py:69-75
+ *   tf_kv_scatter_h2d  load chunks                  tokensim/engine.py:880-888, :607-615
+ *   tf_kv_append / tf_kv_fill_synthetic
+ *                      KV growth of prefill/decode  tokensim/engine.py:484-540
+ *   tf_paged_decode_attn
+ *                      decode_iteration_time        tokensim/costs.py:45-59
+ *                      (as dispatched by _dispatch_gpu, engine.py:669-708)
+ *   tf_policy_tick     BufferAwarePolicy.on_tick    tokensim/scheduler.py:513-772
+ *   tf_policy_fastpath BufferAwarePolicy.opportunistic  scheduler.py:774-809
+ *   tf_iteration_batch BufferAwarePolicy.iteration_batch scheduler.py:811-823
+ *   tf_select_batch    select_batch                 tokensim/scheduler.py:205-269
+ *
+ * Status codes: 0 ok, TF_EINVAL bad arguments, TF_ENOMEM no free block,
+ * TF_EIO CUDA error.  tf_last_error() returns the text of the last failure
+ * on the calling thread.  The Python shim maps them to the reference's
+ * exceptions (ValueError, MemoryError, InvariantError).
+ *
+ * Threading: every launch is asynchronous on the given stream unless noted;
+ * entry points are not re-entrant per pool handle.
+ */
+#ifndef TOKENFLOW_B200_H
+#define TOKENFLOW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TF_OK 0
+#define TF_EINVAL (-22)
+#define TF_ENOMEM (-12)
+#define TF_EIO (-5)
+
+#define TF_DTYPE_BF16 0
+#define TF_TIER_GPU 0
+#define TF_TIER_HOST 1
+#define TF_ENGINE_SM 0 /* SM-driven zero-copy gather/scatter kernel */
+#define TF_ENGINE_CE 1 /* copy engines (cudaMemcpyBatchAsync of contiguous runs) */
+
+const char* tf_last_error(void);
+int tf_abi_version(void);
+
+/* ------------------------------------------------------------------ pool --
+ * Block-major KV layout shared by HBM pool and pinned host store:
+ *   block[b] = [layer][kv(K=0,V=1)][kv_head][slot][head_dim]  (bf16)
+ * so one block (all layers) is one contiguous run of
+ *   n_layers*2*kv_heads*block_tokens*head_dim*2 bytes (2 MiB for Llama3-8B)
+ * and one (block, layer, kv, head) tile is block_tokens*head_dim*2 bytes. */
+int tf_pool_init(void* gpu_pool, int32_t n_blocks, void* host_pool, int32_t n_host_blocks,
+                 int32_t n_layers, int32_t block_tokens, int32_t kv_heads, int32_t head_dim,
+                 int32_t dtype, int64_t* out_handle);
+int tf_pool_destroy(int64_t pool);
+int64_t tf_pool_block_bytes(int64_t pool);
+
+/* Deterministic LIFO block allocator per tier (initial stack [N-1..0]:
+ * block 0 is handed out first).  Host-side bookkeeping, no launch. */
+int tf_blocks_alloc(int64_t pool, int32_t tier, int32_t n, int32_t* out_ids);
+int tf_blocks_free(int64_t pool, int32_t tier, const int32_t* ids, int32_t n);
+int tf_blocks_free_count(int64_t pool, int32_t tier);
+
+/* Device-resident block tables: table[row*row_stride + lb] = physical block.
+ * Applies (row, lb, block|-1) triples (host array) in one launch per 2048. */
+int tf_table_apply(int32_t* dev_table, int32_t row_stride, const int32_t* triples, int32_t n_triples,
+                   void* stream);
+
+/* ------------------------------------------------------------ swap engine --
+ * One segment = n_slots consecutive token slots [slot_begin, slot_begin+n)
+ * of one GPU block <-> the same slots of one host block, for layers
+ * [layer_begin, layer_end).  Segments are passed by value in the launch
+ * (no H2D staging); a whole step's chunks go in one call. */
+typedef struct {
+  int32_t gpu_block;
+  int32_t host_block;
+  int32_t slot_begin;
+  int32_t n_slots;
+} tf_seg;
+
+int tf_kv_gather_d2h(int64_t pool, const tf_seg* segs, int32_t n_segs, int32_t layer_begin, int32_t layer_end,
+                     int32_t engine, void* stream);
+int tf_kv_scatter_h2d(int64_t pool, const tf_seg* segs, int32_t n_segs, int32_t layer_begin, int32_t layer_end,
+                      int32_t engine, void* stream);
+
+/* ---------------------------------------------------------------- KV append --
+ * Model path: write K/V rows of n tokens for one layer, token i at
+ * (table[rows[i]], pos[i]).  k/v: [n][kv_heads][head_dim] bf16 with a row
+ * stride of kv_row_stride elements (so a fused QKV output can be passed). */
+int tf_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride, const int32_t* dev_rows,
+                 const int32_t* dev_pos, int32_t n, int32_t layer, const void* k, const void* v,
+                 int64_t kv_row_stride, void* stream);
+
+/* Synthetic KV (parity / swap benchmarks): positions [pos_begin,pos_end) of
+ * request rid, all layers, value = tf_kv_bits(seed, rid, pos, layer, kv,
+ * head, dim) (identical to oracle/dataplane.py kv_bits). */
+typedef struct {
+  int32_t row;
+  int32_t rid;
+  int32_t pos_begin;
+  int32_t pos_end;
+} tf_span;
+
+int tf_kv_fill_synthetic(int64_t pool, const int32_t* dev_table, int32_t row_stride, const tf_span* spans,
+                         int32_t n_spans, uint32_t seed, void* stream);
+int tf_q_fill_synthetic(void* q, const int32_t* dev_rids, const int32_t* dev_pos, int32_t B, int32_t layer,
+                        int32_t n_q_heads, int32_t head_dim, uint32_t seed, void* stream);
+
+/* ------------------------------------------------------- decode attention --
+ * out[b][h] = softmax(q[b][h] . K[0:ctx[b]]^T * scale) V[0:ctx[b]] over the
+ * paged KV of layer `layer` of request row rows[b]; GQA head h reads kv head
+ * h / (n_q_heads/kv_heads).  q/out: [B][n_q_heads][head_dim] bf16.
+ * fp32 accumulation, split-KV with an in-kernel combine. */
+int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, int32_t row_stride,
+                         const int32_t* dev_rows, const int32_t* dev_ctx, int32_t B, int32_t max_ctx,
+                         int32_t layer, int32_t n_q_heads, float scale, void* out, void* workspace,
+                         int64_t workspace_bytes, void* stream);
+int64_t tf_paged_decode_attn_workspace(int64_t pool, int32_t B, int32_t max_ctx, int32_t n_q_heads);
+
+/* ----------------------------------------------------------------- selector --
+ * Bit-exact GPU restatement of the buffer-aware policy's decisions (IEEE
+ * float64 in the reference's operation order, CPython 3.12 sum() semantics,
+ * glibc exp).  Synchronous: copies in, one single-CTA launch, copies out. */
+typedef struct {
+  int32_t request_id;
+  int32_t prompt_len;
+  int32_t output_len;
+  int32_t running;
+  int32_t pinned;
+  int32_t has_tprime;
+  int64_t generated;
+  int64_t consumed;
+  int64_t ctx_tokens;
+  int64_t gpu_resident;
+  double arrival_time;
+  double rate;
+  double busy_since_tick;
+  double t_io;
+  double t_recompute;
+  double last_iter_time; /* 0.0 encodes None (same truthiness) */
+  double t_prime;        /* policy EMA state (in), ignored unless has_tprime */
+} tf_member;
+
+typedef struct {
+  int32_t request_id;
+  int32_t prompt_len;
+  double waited_s;
+} tf_waiter;
+
+typedef struct {
+  int32_t n_members;
+  int32_t n_waiting;
+  int32_t free_slots;
+  int32_t max_batch;
+  int32_t offload_enabled;
+  int32_t mode; /* in: current policy mode (0 buffer_aware, 1 fcfs_fallback) */
+  int64_t h2d_blocked_tokens;
+  double now;
+  double gpu_mem_free;
+  double gpu_mem_total;
+  double cpu_mem_total;
+  double gamma;
+  /* SchedulerConfig */
+  double schedule_interval;
+  double per_request_mem_estimate;
+  double workingset_adjust_rate;
+  double buffer_safety_factor;
+  double penalty_weight;
+  double tau_schedule;
+  double critical_buffer_seconds;
+  double value_threshold_frac;
+  double value_decay_alpha;
+  double pacing_buffer_seconds;
+  double ema_factor;
+} tf_tick_params;
+
+/* Result arrays (caller-owned host memory, capacity n_members / n_waiting):
+ * counts[0]=mode, [1]=n_preempt, [2]=n_resume, [3]=n_admitted,
+ * [4]=n_recomputed, [5]=n_batches.  resume_how: 0 load, 1 recompute.
+ * batch_sizes[n_batches] partitions batch_ids (prefill sub-batches).
+ * t_prime_out[i] / t_prime_set[i]: EMA state after the tick per member. */
+typedef struct {
+  int32_t* counts;
+  int32_t* preempt;
+  int32_t* resume_ids;
+  int32_t* resume_how;
+  int32_t* admitted;
+  int32_t* recomputed;
+  int32_t* batch_sizes;
+  int32_t* batch_ids;
+  double* t_prime_out;
+  int32_t* t_prime_set;
+} tf_tick_result;
+
+int64_t tf_selector_workspace_bytes(int32_t max_members, int32_t max_waiting);
+int tf_selector_init(void* dev_ws, int64_t dev_bytes, void* host_pinned_ws, int64_t host_bytes, int32_t max_members,
+                     int32_t max_waiting, int64_t* out_handle);
+int tf_selector_destroy(int64_t sel);
+int tf_policy_tick(int64_t sel, const tf_tick_params* p, const tf_member* members, const tf_waiter* waiting,
+                   tf_tick_result* out, void* stream);
+int tf_policy_fastpath(int64_t sel, const tf_tick_params* p, const tf_member* members, const tf_waiter* waiting,
+                       tf_tick_result* out, void* stream);
+
+/* Pacing filter over (id, b_rem, rate) triples -> kept ids (in input order).
+ * Returns the number kept via *n_out. */
+int tf_iteration_batch(int64_t sel, const int32_t* ids, const int64_t* b_rem, const double* rates, int32_t n,
+                       int32_t contention, int32_t mode, double pacing_buffer_seconds, int32_t* out_ids,
+                       int32_t* n_out, void* stream);
+
+/* select_batch on priority views (phi, value, t_prime, rate, utility, length
+ * per candidate) -> chosen flags. */
+typedef struct {
+  int32_t request_id;
+  int32_t pad;
+  int64_t length;
+  double phi;
+  double value;
+  double t_prime;
+  double rate;
+  double utility;
+} tf_prio;
+
+int tf_select_batch(int64_t sel, const tf_prio* views, int32_t n, double gpu_mem, int32_t max_batch,
+                    uint8_t* out_chosen, void* stream);
+
+/* glibc-exact exp, exported for the oracle checks */
+double tf_host_glibc_exp(double x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOKENFLOW_B200_H */

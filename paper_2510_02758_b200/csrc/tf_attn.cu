@@ -1,0 +1,372 @@
+// Paged GQA decode attention over the block-major KV pool.
+//
+// Replaces the reference's affine decode cost (tokensim/costs.py:45-59,
+// dispatched by _dispatch_gpu, tokensim/engine.py:669-708) with the real
+// memory-bound kernel.  Layout: one (block, layer, K|V, kv_head) tile is a
+// contiguous [16 slots][head_dim] bf16 array, so a warp streams a whole tile
+// with one 16-byte load per lane per row pair - fully coalesced, no gather.
+//
+// Work split: CTA = (request b, kv head, KV split); 4 warps, each warp walks
+// every 4th block of its split with its own online-softmax state; the warps
+// merge through shared memory; splits merge in a second tiny kernel.
+// Per block a warp loads K and V (8 KiB for hd=128) up front, computes the
+// G=Hq/Hkv query heads' scores with a butterfly reduce-scatter (30 shuffles
+// instead of 128), and accumulates P.V in fp32.
+#include <float.h>
+
+#include <algorithm>
+
+#include "tf_common.cuh"
+
+namespace tf {
+
+constexpr int kAttnWarps = 4;
+constexpr int kBlk = 16;  // tokens per block (pool block_tokens must be 16)
+
+template <int N>
+struct Pow2Ceil {
+  static constexpr int v = N <= 1 ? 1 : 2 * Pow2Ceil<(N + 1) / 2>::v;
+};
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+struct AttnArgs {
+  const uint16_t* pool;
+  const uint16_t* q;
+  const int32_t* table;
+  const int32_t* rows;
+  const int32_t* ctx;
+  float* ws_acc;  // [B*Hq][splits][D]
+  float* ws_ml;   // [B*Hq][splits][2]
+  uint16_t* out;
+  int64_t block_elems;
+  int32_t stride, n_layers, kv_heads, layer, hq, splits, blocks_per_split;
+  float scale_log2;
+};
+
+// D = head_dim, G = q heads per kv head.
+template <int D, int G>
+__global__ void __launch_bounds__(kAttnWarps * 32) paged_attn_kernel(const AttnArgs a) {
+  constexpr int LPR = D / 8;          // lanes per K/V row (one uint4 each)
+  constexpr int TPP = 32 / LPR;       // rows (tokens) per warp pass
+  constexpr int ITER = kBlk / TPP;    // passes per block
+  constexpr int GP = Pow2Ceil<G>::v > LPR / ITER ? Pow2Ceil<G>::v : LPR / ITER;  // padded head count
+  constexpr int NV = ITER * GP;       // partial scores per lane before reduce
+  constexpr int NR = NV / LPR;        // reduced scores per lane
+  static_assert(NV % LPR == 0 && NR >= 1, "unsupported (D, G)");
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int bh = blockIdx.y;  // b * kv_heads + kvh
+  const int b = bh / a.kv_heads, kvh = bh % a.kv_heads;
+  const int split = blockIdx.x;
+  const int ctx = a.ctx[b];
+  const int nblk = (ctx + kBlk - 1) / kBlk;
+  const int blk_lo = split * a.blocks_per_split;
+  const int blk_hi = min(nblk, blk_lo + a.blocks_per_split);
+  const int col = (lane % LPR) * 8;  // first head dim this lane owns
+  const int rsub = lane / LPR;       // row within a pass
+
+  // q for the lane's 8 dims, all G heads, pre-scaled for exp2
+  float qf[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int h = kvh * G + g;
+    uint4 u = *reinterpret_cast<const uint4*>(a.q + ((int64_t)b * a.hq + h) * D + col);
+    bf16x8_to_f32(u, qf[g]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) qf[g][j] *= a.scale_log2;
+  }
+
+  float m[G], l[G], acc[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    m[g] = -FLT_MAX;
+    l[g] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[g][j] = 0.f;
+  }
+  __shared__ float p_sh[kAttnWarps][kBlk][GP];
+
+  const int32_t* trow = a.table + (int64_t)a.rows[b] * a.stride;
+  const int64_t tile = (int64_t)kBlk * D;
+  const int64_t koff = (((int64_t)a.layer * 2 + 0) * a.kv_heads + kvh) * tile;
+  const int64_t voff = (((int64_t)a.layer * 2 + 1) * a.kv_heads + kvh) * tile;
+
+  for (int blk = blk_lo + warp; blk < blk_hi; blk += kAttnWarps) {
+    const int64_t base = (int64_t)__ldg(trow + blk) * a.block_elems;
+    const uint16_t* kt = a.pool + base + koff;
+    const uint16_t* vt = a.pool + base + voff;
+    uint4 kr[ITER], vr[ITER];
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int t = it * TPP + rsub;
+      kr[it] = __ldg(reinterpret_cast<const uint4*>(kt + t * D + col));
+    }
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int t = it * TPP + rsub;
+      vr[it] = __ldg(reinterpret_cast<const uint4*>(vt + t * D + col));
+    }
+    // partial dot products: val[it*GP + g]
+    float val[NV];
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      float kf[8];
+      bf16x8_to_f32(kr[it], kf);
+#pragma unroll
+      for (int g = 0; g < GP; ++g) {
+        float s = 0.f;
+        if (g < G) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) s = fmaf(qf[g][j], kf[j], s);
+        }
+        val[it * GP + g] = s;
+      }
+    }
+    // butterfly reduce-scatter over the LPR lanes of a row group
+    int cnt = NV;
+#pragma unroll
+    for (int off = LPR / 2; off >= 1; off >>= 1) {
+      const bool upper = (lane & off) != 0;
+      const int half = cnt / 2;
+#pragma unroll
+      for (int i = 0; i < NV / 2; ++i) {
+        if (i < half) {
+          float send = upper ? val[i] : val[i + half];
+          float keep = upper ? val[i + half] : val[i];
+          float recv = __shfl_xor_sync(0xffffffffu, send, off);
+          val[i] = keep + recv;
+        }
+      }
+      cnt = half;
+    }
+    // lane (x = lane % LPR) now owns flat indices x*NR .. x*NR+NR-1
+    const int x = lane % LPR;
+    float bm[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) bm[g] = -FLT_MAX;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int fi = x * NR + r;
+      const int it = fi / GP, g = fi % GP;
+      const int t = it * TPP + rsub;
+      const bool valid = (g < G) && (blk * kBlk + t < ctx);
+      if (!valid) val[r] = -FLT_MAX;
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg)
+        if (g == gg) bm[gg] = fmaxf(bm[gg], val[r]);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) bm[g] = fmaxf(bm[g], __shfl_xor_sync(0xffffffffu, bm[g], off));
+    }
+    float alpha[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float mn = fmaxf(m[g], bm[g]);
+      alpha[g] = exp2f(m[g] - mn);
+      m[g] = mn;
+      l[g] *= alpha[g];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[g][j] *= alpha[g];
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int fi = x * NR + r;
+      const int it = fi / GP, g = fi % GP;
+      const int t = it * TPP + rsub;
+      float p = 0.f;
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg)
+        if (g == gg && val[r] > -FLT_MAX) p = exp2f(val[r] - m[gg]);
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg)
+        if (g == gg) l[gg] += p;
+      p_sh[warp][t][g] = p;
+    }
+    __syncwarp();
+    // P.V for the lane's rows (t = it*TPP + rsub) and dims [col, col+8)
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int t = it * TPP + rsub;
+      if (blk * kBlk + t >= ctx) continue;  // slots past ctx may hold stale bits
+      float vf[8];
+      bf16x8_to_f32(vr[it], vf);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float p = p_sh[warp][t][g];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[g][j] = fmaf(p, vf[j], acc[g][j]);
+      }
+    }
+    __syncwarp();
+  }
+
+  // reduce l over the warp, acc over the TPP row groups
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) l[g] += __shfl_xor_sync(0xffffffffu, l[g], off);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int off = 16; off >= LPR; off >>= 1) acc[g][j] += __shfl_xor_sync(0xffffffffu, acc[g][j], off);
+    }
+  }
+  // merge the warps through shared memory
+  __shared__ float m_sh[kAttnWarps][G], l_sh[kAttnWarps][G];
+  __shared__ float acc_sh[kAttnWarps][G][D];
+  if (lane == 0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      m_sh[warp][g] = m[g];
+      l_sh[warp][g] = l[g];
+    }
+  }
+  if (rsub == 0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc_sh[warp][g][col + j] = acc[g][j];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
+    const int g = e / D, d = e % D;
+    float mm = -FLT_MAX;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) mm = fmaxf(mm, m_sh[w][g]);
+    float ll = 0.f, aa = 0.f;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) {
+      const float f = (m_sh[w][g] == -FLT_MAX) ? 0.f : exp2f(m_sh[w][g] - mm);
+      ll += l_sh[w][g] * f;
+      aa += acc_sh[w][g][d] * f;
+    }
+    const int h = kvh * G + g;
+    const int64_t row = (int64_t)b * a.hq + h;
+    if (a.splits == 1) {
+      const float o = ll > 0.f ? aa / ll : 0.f;
+      a.out[row * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(o));
+    } else {
+      a.ws_acc[(row * a.splits + split) * D + d] = aa;
+      if (d == 0) {
+        a.ws_ml[(row * a.splits + split) * 2 + 0] = mm;
+        a.ws_ml[(row * a.splits + split) * 2 + 1] = ll;
+      }
+    }
+  }
+}
+
+// one CTA per (b, q head): merge the splits
+template <int D>
+__global__ void attn_combine_kernel(const AttnArgs a) {
+  const int64_t row = blockIdx.x;
+  float mm = -FLT_MAX;
+  for (int s = 0; s < a.splits; ++s) mm = fmaxf(mm, a.ws_ml[(row * a.splits + s) * 2]);
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float ll = 0.f, aa = 0.f;
+    for (int s = 0; s < a.splits; ++s) {
+      const float ms = a.ws_ml[(row * a.splits + s) * 2];
+      if (ms == -FLT_MAX) continue;
+      const float f = exp2f(ms - mm);
+      ll += a.ws_ml[(row * a.splits + s) * 2 + 1] * f;
+      aa += a.ws_acc[(row * a.splits + s) * D + d] * f;
+    }
+    a.out[row * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(ll > 0.f ? aa / ll : 0.f));
+  }
+}
+
+static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps) {
+  const int nblk = std::max(1, (max_ctx + kBlk - 1) / kBlk);
+  const int base = std::max(1, B * kv_heads);
+  const int target = 148 * 6;  // resident CTAs per wave (4 warps each)
+  int s = std::max(1, std::min((target + base - 1) / base, (nblk + 7) / 8));
+  int per = (nblk + s - 1) / s;
+  s = (nblk + per - 1) / per;
+  *splits = s;
+  *bps = per;
+}
+
+template <int D, int G>
+static int launch(const AttnArgs& a, int B, cudaStream_t st) {
+  dim3 grid(a.splits, B * a.kv_heads);
+  paged_attn_kernel<D, G><<<grid, kAttnWarps * 32, 0, st>>>(a);
+  TF_LAUNCH_CHECK();
+  if (a.splits > 1) {
+    attn_combine_kernel<D><<<B * a.hq, std::min(D, 128), 0, st>>>(a);
+    TF_LAUNCH_CHECK();
+  }
+  return TF_OK;
+}
+
+}  // namespace tf
+
+using namespace tf;
+
+extern "C" {
+
+int64_t tf_paged_decode_attn_workspace(int64_t pool, int32_t B, int32_t max_ctx, int32_t n_q_heads) {
+  Pool* p = get_pool(pool);
+  if (!p) return -1;
+  int splits, bps;
+  plan_splits(B, p->kv_heads, max_ctx, &splits, &bps);
+  if (splits == 1) return 0;
+  return (int64_t)B * n_q_heads * splits * (p->head_dim + 2) * (int64_t)sizeof(float);
+}
+
+int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, int32_t row_stride,
+                         const int32_t* dev_rows, const int32_t* dev_ctx, int32_t B, int32_t max_ctx, int32_t layer,
+                         int32_t n_q_heads, float scale, void* out, void* workspace, int64_t workspace_bytes,
+                         void* stream) {
+  Pool* p = get_pool(pool);
+  TF_CHECK_ARG(p, "tf_paged_decode_attn: unknown pool");
+  TF_CHECK_ARG(p->block_tokens == kBlk, "tf_paged_decode_attn: block_tokens must be 16");
+  TF_CHECK_ARG(layer >= 0 && layer < p->n_layers, "tf_paged_decode_attn: bad layer");
+  TF_CHECK_ARG(n_q_heads % p->kv_heads == 0, "tf_paged_decode_attn: n_q_heads %% kv_heads != 0");
+  TF_CHECK_ARG(B >= 0 && max_ctx >= 0, "tf_paged_decode_attn: bad B/max_ctx");
+  if (B == 0) return TF_OK;
+  TF_CHECK_ARG(q && dev_table && dev_rows && dev_ctx && out, "tf_paged_decode_attn: NULL pointer");
+  AttnArgs a;
+  a.pool = p->gpu;
+  a.q = (const uint16_t*)q;
+  a.table = dev_table;
+  a.rows = dev_rows;
+  a.ctx = dev_ctx;
+  a.out = (uint16_t*)out;
+  a.block_elems = p->block_elems;
+  a.stride = row_stride;
+  a.n_layers = p->n_layers;
+  a.kv_heads = p->kv_heads;
+  a.layer = layer;
+  a.hq = n_q_heads;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  plan_splits(B, p->kv_heads, max_ctx, &a.splits, &a.blocks_per_split);
+  int64_t need = a.splits == 1 ? 0 : (int64_t)B * n_q_heads * a.splits * (p->head_dim + 2) * (int64_t)sizeof(float);
+  TF_CHECK_ARG(workspace_bytes >= need && (need == 0 || workspace), "tf_paged_decode_attn: workspace too small (%lld < %lld)",
+               (long long)workspace_bytes, (long long)need);
+  a.ws_acc = (float*)workspace;
+  a.ws_ml = a.ws_acc + (int64_t)B * n_q_heads * a.splits * p->head_dim;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int G = n_q_heads / p->kv_heads;
+  const int D = p->head_dim;
+  if (D == 128 && G == 4) return launch<128, 4>(a, B, st);
+  if (D == 128 && G == 5) return launch<128, 5>(a, B, st);
+  if (D == 128 && G == 8) return launch<128, 8>(a, B, st);
+  if (D == 128 && G == 2) return launch<128, 2>(a, B, st);
+  if (D == 128 && G == 1) return launch<128, 1>(a, B, st);
+  if (D == 64 && G == 2) return launch<64, 2>(a, B, st);
+  if (D == 64 && G == 4) return launch<64, 4>(a, B, st);
+  if (D == 64 && G == 1) return launch<64, 1>(a, B, st);
+  set_error("tf_paged_decode_attn: unsupported head_dim %d / group %d", D, G);
+  return TF_EINVAL;
+}
+
+}  // extern "C"

@@ -1,0 +1,220 @@
+// Swap engine: token-granular paged KV movement between the HBM pool and the
+// pinned host store.
+//
+// Replaces the reference's simulated PCIe channels (tokensim/engine.py:235-247,
+// :736-779) and transfer_time (tokensim/costs.py:69-75): a write-through /
+// evict chunk becomes one gather (HBM -> host), a load chunk one scatter
+// (host -> HBM).  Two engines:
+//   TF_ENGINE_SM  - SM-driven zero-copy kernel: 16-byte vectorised, fully
+//                   coalesced reads of the block-major pool, posted writes
+//                   straight into mapped pinned memory (d2h) or deep batches
+//                   of outstanding sysmem loads (h2d).  Grid capped to a few
+//                   dozen CTAs: PCIe, not the SMs, is the bound, and the
+//                   decode step keeps the rest of the machine.
+//   TF_ENGINE_CE  - copy engines: the segments are coalesced into maximal
+//                   contiguous runs (a whole block of all layers is a single
+//                   2 MiB run in this layout) and submitted as ONE
+//                   cudaMemcpyBatchAsync; no SM is used at all.
+#include <algorithm>
+
+#include "tf_common.cuh"
+
+namespace tf {
+
+constexpr int kMaxSegs = 1536;
+constexpr int kSwapThreads = 256;
+constexpr int kUnroll = 8;
+
+struct SwapArgs {
+  PoolView pv;
+  int32_t layer_begin, layer_end, n_segs, to_host;
+  int32_t gpu_block[kMaxSegs];
+  int32_t host_block[kMaxSegs];
+  int16_t slot_begin[kMaxSegs];
+  int16_t n_slots[kMaxSegs];
+};
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint4 ld_sysmem(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// blockIdx.y = segment; the segment's vectors (16 B) are enumerated as
+// run-major (layer, kv, head) x (slot, dim/8) and strided over blockIdx.x.
+__global__ void __launch_bounds__(kSwapThreads) swap_kernel(const __grid_constant__ SwapArgs a) {
+  const int s = blockIdx.y;
+  const PoolView& pv = a.pv;
+  const int ns = a.n_slots[s];
+  const int vpr = ns * pv.head_dim / 8;            // vectors per run
+  const int runs = (a.layer_end - a.layer_begin) * 2 * pv.kv_heads;
+  const int64_t total = (int64_t)runs * vpr;
+  const int64_t gb = a.gpu_block[s], hb = a.host_block[s];
+  const int sb = a.slot_begin[s];
+  const int64_t stride = (int64_t)gridDim.x * kSwapThreads;
+  for (int64_t v0 = (int64_t)blockIdx.x * kSwapThreads + threadIdx.x; v0 < total; v0 += stride * kUnroll) {
+    uint4 buf[kUnroll];
+    int64_t dst_off[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      int64_t v = v0 + (int64_t)u * stride;
+      dst_off[u] = -1;
+      if (v < total) {
+        int rho = (int)(v / vpr), i = (int)(v - (int64_t)rho * vpr);
+        int l = a.layer_begin + rho / (2 * pv.kv_heads);
+        int kv = (rho / pv.kv_heads) & 1, h = rho % pv.kv_heads;
+        int64_t g = pv.off(gb, l, kv, h, sb) + (int64_t)i * 8;
+        int64_t c = pv.off(hb, l, kv, h, sb) + (int64_t)i * 8;
+        if (a.to_host) {
+          buf[u] = ld_stream(reinterpret_cast<const uint4*>(pv.gpu + g));
+          dst_off[u] = c;
+        } else {
+          buf[u] = ld_sysmem(reinterpret_cast<const uint4*>(pv.host + c));
+          dst_off[u] = g;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (dst_off[u] >= 0) {
+        uint16_t* base = a.to_host ? pv.host : pv.gpu;
+        st_stream(reinterpret_cast<uint4*>(base + dst_off[u]), buf[u]);
+      }
+    }
+  }
+}
+
+static int swap_sm(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int to_host,
+                   cudaStream_t st) {
+  for (int32_t base = 0; base < n; base += kMaxSegs) {
+    SwapArgs a;
+    a.pv = view_of(p);
+    a.layer_begin = l0;
+    a.layer_end = l1;
+    a.to_host = to_host;
+    a.n_segs = std::min<int32_t>(kMaxSegs, n - base);
+    int64_t max_vec = 0, tot_vec = 0;
+    for (int i = 0; i < a.n_segs; ++i) {
+      const tf_seg& s = segs[base + i];
+      a.gpu_block[i] = s.gpu_block;
+      a.host_block[i] = s.host_block;
+      a.slot_begin[i] = (int16_t)s.slot_begin;
+      a.n_slots[i] = (int16_t)s.n_slots;
+      int64_t v = (int64_t)(l1 - l0) * 2 * p.kv_heads * s.n_slots * p.head_dim / 8;
+      max_vec = std::max(max_vec, v);
+      tot_vec += v;
+    }
+    // PCIe-bound: ~128 CTAs of 256 threads x 8 x 16 B keep > 4 MB in flight.
+    int64_t want = (max_vec + (int64_t)kSwapThreads * kUnroll - 1) / ((int64_t)kSwapThreads * kUnroll);
+    int64_t cap = std::max<int64_t>(1, 128 / std::max<int32_t>(1, a.n_segs));
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, cap)), (unsigned)a.n_segs);
+    swap_kernel<<<grid, kSwapThreads, 0, st>>>(a);
+    TF_LAUNCH_CHECK();
+    (void)tot_vec;
+  }
+  return TF_OK;
+}
+
+// Copy-engine path: maximal contiguous runs, one batched submission.
+static int swap_ce(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int to_host,
+                   cudaStream_t st) {
+  std::vector<void*> dst, src;
+  std::vector<size_t> sz;
+  const bool all_layers = (l0 == 0 && l1 == p.n_layers);
+  auto push = [&](int64_t goff, int64_t hoff, int64_t elems) {
+    uint16_t* g = p.gpu + goff;
+    uint16_t* h = p.host + hoff;
+    size_t bytes = (size_t)elems * 2;
+    // merge with the previous run when both sides continue contiguously
+    if (!sz.empty()) {
+      char* pd = (char*)dst.back() + sz.back();
+      char* ps = (char*)src.back() + sz.back();
+      if (pd == (char*)(to_host ? (void*)h : (void*)g) && ps == (char*)(to_host ? (void*)g : (void*)h)) {
+        sz.back() += bytes;
+        return;
+      }
+    }
+    dst.push_back(to_host ? (void*)h : (void*)g);
+    src.push_back(to_host ? (void*)g : (void*)h);
+    sz.push_back(bytes);
+  };
+  for (int32_t i = 0; i < n; ++i) {
+    const tf_seg& s = segs[i];
+    if (all_layers && s.n_slots == p.block_tokens && s.slot_begin == 0) {
+      push(p.off(s.gpu_block, 0, 0, 0, 0), p.off(s.host_block, 0, 0, 0, 0), p.block_elems);
+      continue;
+    }
+    for (int l = l0; l < l1; ++l)
+      for (int kv = 0; kv < 2; ++kv)
+        for (int h = 0; h < p.kv_heads; ++h)
+          push(p.off(s.gpu_block, l, kv, h, s.slot_begin), p.off(s.host_block, l, kv, h, s.slot_begin),
+               (int64_t)s.n_slots * p.head_dim);
+  }
+  if (sz.empty()) return TF_OK;
+  cudaMemcpyAttributes attr;
+  memset(&attr, 0, sizeof(attr));
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  attr.srcLocHint.type = to_host ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
+  attr.dstLocHint.type = to_host ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
+  size_t attr_idx = 0, fail = 0;
+  cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), sz.size(), &attr, &attr_idx, 1, &fail, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    // Fall back to individual async copies (same engines, more submissions).
+    for (size_t i = 0; i < sz.size(); ++i)
+      TF_CUDA(cudaMemcpyAsync(dst[i], src[i], sz[i], to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st));
+  }
+  return TF_OK;
+}
+
+static int swap_entry(int64_t pool, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int32_t engine,
+                      int to_host, void* stream) {
+  Pool* p = get_pool(pool);
+  TF_CHECK_ARG(p, "swap: unknown pool");
+  TF_CHECK_ARG(p->host && p->gpu, "swap: pool has no host tier");
+  TF_CHECK_ARG(n >= 0 && (n == 0 || segs), "swap: bad segment list");
+  TF_CHECK_ARG(0 <= l0 && l0 < l1 && l1 <= p->n_layers, "swap: bad layer range [%d,%d)", l0, l1);
+  for (int32_t i = 0; i < n; ++i) {
+    const tf_seg& s = segs[i];
+    TF_CHECK_ARG(s.gpu_block >= 0 && s.gpu_block < p->n_blocks, "swap: gpu block %d out of range", s.gpu_block);
+    TF_CHECK_ARG(s.host_block >= 0 && s.host_block < p->n_host_blocks, "swap: host block %d out of range",
+                 s.host_block);
+    TF_CHECK_ARG(s.slot_begin >= 0 && s.n_slots > 0 && s.slot_begin + s.n_slots <= p->block_tokens,
+                 "swap: bad slot range [%d,+%d)", s.slot_begin, s.n_slots);
+  }
+  if (n == 0) return TF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (engine == TF_ENGINE_CE) return swap_ce(*p, segs, n, l0, l1, to_host, st);
+  TF_CHECK_ARG(engine == TF_ENGINE_SM, "swap: unknown engine %d", engine);
+  return swap_sm(*p, segs, n, l0, l1, to_host, st);
+}
+
+}  // namespace tf
+
+extern "C" {
+
+int tf_kv_gather_d2h(int64_t pool, const tf_seg* segs, int32_t n_segs, int32_t layer_begin, int32_t layer_end,
+                     int32_t engine, void* stream) {
+  return tf::swap_entry(pool, segs, n_segs, layer_begin, layer_end, engine, 1, stream);
+}
+
+int tf_kv_scatter_h2d(int64_t pool, const tf_seg* segs, int32_t n_segs, int32_t layer_begin, int32_t layer_end,
+                      int32_t engine, void* stream) {
+  return tf::swap_entry(pool, segs, n_segs, layer_begin, layer_end, engine, 0, stream);
+}
+
+}  // extern "C"

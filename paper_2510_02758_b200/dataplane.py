@@ -1,0 +1,453 @@
+"""GPU data plane: paged KV block manager + swap engine + decode step.
+
+Owns the KV pool in HBM, the pinned host store, the device-resident block
+tables and the copy streams, and turns every token-count transition of the
+engine (engine.py here, tokensim/engine.py in the reference) into real work
+through the C ABI (_tf_b200.so):
+
+  transition (reference)                        GPU work
+  prefill dispatch        engine.py:669-692     block alloc + KV write
+  decode dispatch         engine.py:693-708     block alloc + KV append + paged attention
+  write-through / evict   engine.py:781-848     tf_kv_gather_d2h on the evict stream
+  load                    engine.py:850-888     tf_kv_scatter_h2d on the load stream
+  preempt instant release kvstore.py:144-154    block frees
+  recompute / done        engine.py:542-557, :889-917  block frees
+
+Token-range semantics (which positions each count refers to) are the
+canonical ones written down in DESIGN.md and restated independently by
+oracle/dataplane.py; block tables and bytes must match it bit for bit.
+
+Pool layout (block-major): block[b] = [layer][K|V][kv_head][slot][head_dim]
+bf16, identical in HBM and in the pinned host store, so a full block of all
+layers moves as one contiguous 2 MiB run (Llama3-8B).
+
+Modes
+  replay    one CUDA stream for everything: program order is stream order,
+            so every hazard (free-then-reuse, load-after-evict) is ordered
+            by construction; used for bit-exact parity runs.
+  realtime  compute / evict (d2h) / load (h2d) streams overlapped; block
+            frees are fenced by CUDA events before reuse, loads of a range
+            wait on the eviction that produced it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from collections import deque
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import TIER_GPU, TIER_HOST, TfSeg, TfSpan, check, lib
+
+LIVE, DETACHED, RESERVED = np.uint8(1), np.uint8(2), np.uint8(4)
+CLR_LIVE, CLR_DETACHED, CLR_RESERVED = np.uint8(0xFE), np.uint8(0xFD), np.uint8(0xFB)
+
+
+def _i32(a) -> C.Array:
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    return (C.c_int32 * max(1, a.size)).from_buffer_copy(a.tobytes() if a.size else b"\0\0\0\0")
+
+
+class KvPool:
+    """HBM pool + pinned host store + C-ABI pool handle."""
+
+    def __init__(self, n_blocks, n_host_blocks, n_layers, kv_heads, head_dim, block_tokens=16, device="cuda"):
+        self.n_blocks, self.n_host_blocks = n_blocks, n_host_blocks
+        self.L, self.H, self.D, self.B = n_layers, kv_heads, head_dim, block_tokens
+        self.block_elems = n_layers * 2 * kv_heads * block_tokens * head_dim
+        self.device = torch.device(device)
+        self.gpu = torch.empty(n_blocks * self.block_elems, dtype=torch.int16, device=self.device)
+        self.host = torch.empty(max(1, n_host_blocks) * self.block_elems, dtype=torch.int16, pin_memory=True)
+        h = C.c_int64()
+        check(lib.tf_pool_init(C.c_void_p(self.gpu.data_ptr()), n_blocks, C.c_void_p(self.host.data_ptr()),
+                               n_host_blocks, n_layers, block_tokens, kv_heads, head_dim, 0, C.byref(h)),
+              "tf_pool_init")
+        self.handle = h.value
+
+    @property
+    def block_bytes(self) -> int:
+        return self.block_elems * 2
+
+    def alloc(self, tier: int, n: int) -> list:
+        if n == 0:
+            return []
+        out = (C.c_int32 * n)()
+        check(lib.tf_blocks_alloc(self.handle, tier, n, out), "tf_blocks_alloc")
+        return list(out)
+
+    def free(self, tier: int, ids) -> None:
+        ids = list(ids)
+        if ids:
+            check(lib.tf_blocks_free(self.handle, tier, _i32(ids), len(ids)), "tf_blocks_free")
+
+    def free_count(self, tier: int) -> int:
+        return lib.tf_blocks_free_count(self.handle, tier)
+
+    def gpu_view(self) -> torch.Tensor:
+        """[n_blocks, L, 2, H, B, D] int16 view of the HBM pool (bf16 bits)."""
+        return self.gpu.view(self.n_blocks, self.L, 2, self.H, self.B, self.D)
+
+    def host_view(self) -> torch.Tensor:
+        return self.host[: self.n_host_blocks * self.block_elems].view(self.n_host_blocks, self.L, 2, self.H, self.B,
+                                                                        self.D)
+
+    def close(self):
+        if self.handle:
+            lib.tf_pool_destroy(self.handle)
+            self.handle = 0
+
+
+class GpuDataPlane:
+    """Engine hooks -> block manager bookkeeping + kernel launches."""
+
+    def __init__(self, reqs, pool: KvPool, mode: str = "replay", kv_source: str = "synthetic", seed: int = 0,
+                 attention: str = "all", engine: int = _lib.ENGINE_SM, model=None, n_q_heads: int | None = None):
+        assert mode in ("replay", "realtime")
+        self.pool, self.mode, self.kv_source, self.seed = pool, mode, kv_source, seed
+        self.attention = attention  # "all" layers, "none", or an int layer count
+        self.swap_engine = engine
+        self.model = model
+        self.n_q_heads = n_q_heads or 2 * pool.H
+        self.B = pool.B
+        dev = pool.device
+        self.max_len = max(r.prompt_len + r.output_len + 2 for r in reqs)
+        self.nlb = (self.max_len + self.B - 1) // self.B
+        n_rows = max(r.id for r in reqs) + 1
+        self.flags = {r.id: np.zeros(self.nlb * self.B, np.uint8) for r in reqs}
+        self.gtab = {r.id: np.full(self.nlb, -1, np.int32) for r in reqs}
+        self.htab = {r.id: np.full(self.nlb, -1, np.int32) for r in reqs}
+        self.host_hi = {r.id: 0 for r in reqs}
+        self.table = torch.full((n_rows, self.nlb), -1, dtype=torch.int32, device=dev)
+        if mode == "replay":
+            self.s_compute = self.s_evict = self.s_load = torch.cuda.Stream(device=dev)
+        else:
+            self.s_compute = torch.cuda.Stream(device=dev)
+            self.s_evict = torch.cuda.Stream(device=dev)
+            self.s_load = torch.cuda.Stream(device=dev)
+        self._pending_table = []  # (row, lb, block) not yet applied on device
+        self._d2h_busy = None  # (rid, lo, hi, kind, event)
+        self._last_d2h_event = {}  # rid -> event of its last d2h (loads of that range wait on it)
+        self._quarantine: deque = deque()  # (event, [blocks]) realtime frees awaiting their fence
+        self.peak_blocks = 0
+        self.peak_host_blocks = 0
+        self.stats = {"d2h_tokens": 0, "h2d_tokens": 0, "d2h_launches": 0, "h2d_launches": 0, "append_tokens": 0,
+                      "fill_tokens": 0, "attn_launches": 0, "decode_steps": 0}
+        self._events = []  # (kind, tokens, start_evt, end_evt) for measured transfer rates
+        ws = max(1, int(lib.tf_paged_decode_attn_workspace(pool.handle, max(1, len(reqs)), self.max_len, 64)))
+        self._attn_ws = torch.empty(ws, dtype=torch.uint8, device=dev)
+        self.attn_out = None
+
+    # ------------------------------------------------------------ block table
+    def _reconcile(self, rid, blocks):
+        f, tab = self.flags[rid], self.gtab[rid]
+        blocks = sorted(set(int(j) for j in blocks))
+        occ = [bool(f[j * self.B:(j + 1) * self.B].any()) for j in blocks]
+        freed = []
+        for j, o in zip(blocks, occ):
+            if not o and tab[j] >= 0:
+                freed.append(int(tab[j]))
+                tab[j] = -1
+                self._pending_table.append((rid, j, -1))
+        if freed:
+            self._release_blocks(freed)
+        need = [j for j, o in zip(blocks, occ) if o and tab[j] < 0]
+        if need:
+            ids = self._alloc_blocks(len(need))
+            for j, b in zip(need, ids):
+                tab[j] = b
+                self._pending_table.append((rid, j, b))
+        used = self.pool.n_blocks - self.pool.free_count(TIER_GPU) - sum(len(b) for _, b in self._quarantine)
+        self.peak_blocks = max(self.peak_blocks, used)
+
+    def _release_blocks(self, ids):
+        if self.mode == "replay":
+            self.pool.free(TIER_GPU, ids)
+        else:
+            ev = torch.cuda.Event()
+            ev.record(self.s_compute)
+            self._quarantine.append((ev, ids))
+
+    def _alloc_blocks(self, n):
+        if self.mode == "realtime":
+            while self._quarantine and self._quarantine[0][0].query():
+                self.pool.free(TIER_GPU, self._quarantine.popleft()[1])
+            if self.pool.free_count(TIER_GPU) < n:
+                while self._quarantine and self.pool.free_count(TIER_GPU) < n:
+                    ev, ids = self._quarantine.popleft()
+                    ev.synchronize()
+                    self.pool.free(TIER_GPU, ids)
+        return self.pool.alloc(TIER_GPU, n)
+
+    def _flush_table(self, stream):
+        if not self._pending_table:
+            return
+        t = np.asarray(self._pending_table, np.int32).reshape(-1)
+        self._pending_table = []
+        check(lib.tf_table_apply(C.c_void_p(self.table.data_ptr()), self.nlb, _i32(t), len(t) // 3,
+                                 C.c_void_p(stream.cuda_stream)), "tf_table_apply")
+
+    def _segments(self, rid, positions, host=True):
+        """Group sorted positions into per-block slot runs -> TfSeg array."""
+        segs = []
+        if len(positions) == 0:
+            return segs
+        p = np.asarray(positions)
+        br = np.nonzero(np.diff(p) != 1)[0] + 1
+        for run in np.split(p, br):
+            lo, hi = int(run[0]), int(run[-1]) + 1
+            while lo < hi:
+                j = lo // self.B
+                e = min(hi, (j + 1) * self.B)
+                segs.append((int(self.gtab[rid][j]), int(self.htab[rid][j]) if host else -1, lo - j * self.B, e - lo))
+                lo = e
+        return segs
+
+    @staticmethod
+    def _seg_array(segs):
+        arr = (TfSeg * max(1, len(segs)))()
+        for i, (g, h, s, n) in enumerate(segs):
+            arr[i].gpu_block, arr[i].host_block, arr[i].slot_begin, arr[i].n_slots = g, h, s, n
+        return arr
+
+    # ------------------------------------------------------------ KV writes
+    def _write_kv(self, spans, stream):
+        """spans: (rid, lo, hi) positions whose KV is produced now."""
+        if not spans:
+            return
+        self._flush_table(stream)
+        if self.kv_source == "synthetic":
+            stream = self.s_compute
+            arr = (TfSpan * len(spans))()
+            for i, (rid, lo, hi) in enumerate(spans):
+                arr[i].row, arr[i].rid, arr[i].pos_begin, arr[i].pos_end = rid, rid, lo, hi
+            check(lib.tf_kv_fill_synthetic(self.pool.handle, C.c_void_p(self.table.data_ptr()), self.nlb, arr,
+                                           len(spans), self.seed, C.c_void_p(stream.cuda_stream)),
+                  "tf_kv_fill_synthetic")
+
+    # ------------------------------------------------------------ engine hooks
+    def fill_start(self, job, eng):
+        spans = []
+        for rid in job.members:
+            tot = eng.state[rid].kv.total_kv
+            lo = 0 if job.kind == "recompute" else tot
+            hi = lo + job.reserve[rid]
+            f = self.flags[rid]
+            if (f[lo:hi] & (LIVE | RESERVED)).any():
+                raise _lib.InvariantError(f"prefill of {rid} overlaps resident KV")
+            f[lo:hi] |= RESERVED
+            self._reconcile(rid, range(lo // self.B, (hi - 1) // self.B + 1))
+            spans.append((rid, lo, hi))
+            self.stats["fill_tokens"] += hi - lo
+        self._wait_d2h_of(spans, self.s_compute)
+        if self.model is not None and self.kv_source == "model":
+            self._flush_table(self.s_compute)
+            self.model.prefill(self, job, spans, eng)
+        else:
+            self._write_kv(spans, self.s_compute)
+
+    def fill_done(self, rid):
+        f = self.flags[rid]
+        m = (f & RESERVED) != 0
+        f[m] = (f[m] & CLR_RESERVED) | LIVE
+
+    def decode_start(self, batch, eng):
+        spans = []
+        for rid in batch:
+            p = eng.state[rid].kv.total_kv
+            f = self.flags[rid]
+            if eng.debug_checks and not (f[:p] & LIVE).all():
+                raise _lib.InvariantError(f"decode of {rid} reads non-resident KV")
+            f[p] |= RESERVED
+            if p % self.B == 0 or self.gtab[rid][p // self.B] < 0:
+                self._reconcile(rid, [p // self.B])
+            spans.append((rid, p, p + 1))
+        self.stats["append_tokens"] += len(batch)
+        self.stats["decode_steps"] += 1
+        self._wait_d2h_of(spans, self.s_compute)
+        if self.model is not None and self.kv_source == "model":
+            self._flush_table(self.s_compute)
+            self.model.decode(self, batch, eng)
+        else:
+            self._write_kv(spans, self.s_compute)
+            self._synthetic_attention(batch, eng)
+
+    def decode_done(self, batch, made):
+        made = set(made)
+        for rid in batch:
+            f = self.flags[rid]
+            idx = np.nonzero(f & RESERVED)[0]
+            if rid in made:
+                f[idx] = (f[idx] & CLR_RESERVED) | LIVE
+            else:
+                f[idx] &= CLR_RESERVED
+                self._reconcile(rid, {int(i) // self.B for i in idx})
+
+    def d2h_start(self, ch, eng):
+        rid = ch.owner
+        cs = eng.state[rid].kv.cpu_synced
+        lo, hi = cs, cs + ch.tokens
+        f = self.flags[rid]
+        if not (f[lo:hi] & LIVE).all():
+            raise _lib.InvariantError(f"d2h of {rid} [{lo},{hi}) reads non-resident KV")
+        htab = self.htab[rid]
+        need = [j for j in range(lo // self.B, (hi - 1) // self.B + 1) if htab[j] < 0]
+        for j, b in zip(need, self.pool.alloc(TIER_HOST, len(need))):
+            htab[j] = b
+        self.peak_host_blocks = max(self.peak_host_blocks, self.pool.n_host_blocks - self.pool.free_count(TIER_HOST))
+        self.host_hi[rid] = max(self.host_hi[rid], hi)
+        segs = self._segments(rid, np.arange(lo, hi))
+        st = self.s_evict
+        if self.mode == "realtime":
+            st.wait_stream(self.s_compute)  # positions appended by finished decodes
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        check(lib.tf_kv_gather_d2h(self.pool.handle, self._seg_array(segs), len(segs), 0, self.pool.L,
+                                   self.swap_engine, C.c_void_p(st.cuda_stream)), "tf_kv_gather_d2h")
+        t1.record(st)
+        self._events.append(("d2h", ch.tokens, t0, t1))
+        if ch.kind == "evict":
+            f[lo:hi] = (f[lo:hi] & CLR_LIVE) | DETACHED
+        self._d2h_busy = (rid, lo, hi, ch.kind, t1)
+        self._last_d2h_event[rid] = t1
+        self.stats["d2h_tokens"] += ch.tokens
+        self.stats["d2h_launches"] += 1
+
+    def d2h_done(self, ch, alive):
+        rid, lo, hi, kind, ev = self._d2h_busy
+        self._d2h_busy = None
+        if kind == "evict":
+            self.flags[rid][lo:hi] &= CLR_DETACHED
+            if self.mode == "realtime":
+                ev.synchronize()
+            self._reconcile(rid, range(lo // self.B, (hi - 1) // self.B + 1))
+
+    def h2d_start(self, ch, eng):
+        rid = ch.owner
+        tot = eng.state[rid].kv.total_kv
+        f = self.flags[rid]
+        miss = np.nonzero((f[:tot] & LIVE) == 0)[0][: ch.tokens]
+        if len(miss) != ch.tokens or (len(miss) and miss[-1] >= self.host_hi[rid]):
+            raise _lib.InvariantError(f"load of {rid} needs positions missing from the host store")
+        f[miss] |= LIVE
+        self._reconcile(rid, {int(p) // self.B for p in miss})
+        st = self.s_load
+        ev = self._last_d2h_event.get(rid)
+        if self.mode == "realtime" and ev is not None:
+            st.wait_event(ev)
+        segs = self._segments(rid, miss)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        check(lib.tf_kv_scatter_h2d(self.pool.handle, self._seg_array(segs), len(segs), 0, self.pool.L,
+                                    self.swap_engine, C.c_void_p(st.cuda_stream)), "tf_kv_scatter_h2d")
+        t1.record(st)
+        self._events.append(("h2d", ch.tokens, t0, t1))
+        self.stats["h2d_tokens"] += ch.tokens
+        self.stats["h2d_launches"] += 1
+        if self.mode == "realtime":
+            self.s_compute.wait_event(t1)
+
+    def release_prefix(self, rid, n):
+        f = self.flags[rid]
+        idx = np.nonzero(f & LIVE)[0][:n]
+        if len(idx) != n:
+            raise _lib.InvariantError(f"instant release of {n} tokens but {len(idx)} resident")
+        f[idx] &= CLR_LIVE
+        self._reconcile(rid, {int(i) // self.B for i in idx})
+
+    def cancel_evicts(self, rid):
+        pass
+
+    def drop_gpu(self, rid):
+        f = self.flags[rid]
+        idx = np.nonzero(f & LIVE)[0]
+        f[idx] &= CLR_LIVE
+        self._reconcile(rid, {int(i) // self.B for i in idx})
+
+    def drop_host(self, rid):
+        tab = self.htab[rid]
+        ids = [int(b) for b in tab if b >= 0]
+        tab[:] = -1
+        self.pool.free(TIER_HOST, ids)
+        self.host_hi[rid] = 0
+
+    def finish(self, rid):
+        f = self.flags[rid]
+        idx = np.nonzero(f)[0]
+        f[:] = 0
+        self._reconcile(rid, {int(i) // self.B for i in idx})
+        self.drop_host(rid)
+
+    def audit(self, eng):
+        for rid, s in eng.state.items():
+            if s.status in ("gen_done", "done"):
+                continue
+            f = self.flags[rid]
+            fly = eng.h2d.in_service.tokens if (eng.h2d.in_service is not None and eng.h2d.in_service.owner == rid) else 0
+            n = int(np.count_nonzero(f & LIVE)) + int(np.count_nonzero(f & DETACHED))
+            if n != s.kv.gpu_resident + fly:
+                raise _lib.InvariantError(f"request {rid}: {n} resident positions vs ledger {s.kv.gpu_resident}+{fly}")
+
+    def _wait_d2h_of(self, spans, stream):
+        if self.mode != "realtime":
+            return
+        for rid, _, _ in spans:
+            busy = self._d2h_busy
+            if busy is not None and busy[0] == rid:
+                stream.wait_event(busy[4])
+
+    # ------------------------------------------------------------ attention
+    def _synthetic_attention(self, batch, eng):
+        """Decode attention over each member's paged KV (synthetic q)."""
+        if self.attention == "none" or not batch:
+            return
+        n_layers = self.pool.L if self.attention == "all" else int(self.attention)
+        st = self.s_compute
+        B = len(batch)
+        rows = torch.tensor(list(batch), dtype=torch.int32).pin_memory().to(self.pool.device, non_blocking=True)
+        pos = [eng.state[r].kv.total_kv for r in batch]
+        ctx = torch.tensor([p + 1 for p in pos], dtype=torch.int32).pin_memory().to(self.pool.device,
+                                                                                      non_blocking=True)
+        posd = torch.tensor(pos, dtype=torch.int32).pin_memory().to(self.pool.device, non_blocking=True)
+        hq = self.n_q_heads
+        q = torch.empty((B, hq, self.pool.D), dtype=torch.int16, device=self.pool.device)
+        out = torch.empty_like(q)
+        ws_need = int(lib.tf_paged_decode_attn_workspace(self.pool.handle, B, max(pos) + 1, hq))
+        if ws_need > self._attn_ws.numel():
+            self._attn_ws = torch.empty(ws_need, dtype=torch.uint8, device=self.pool.device)
+        scale = 1.0 / float(self.pool.D) ** 0.5
+        with torch.cuda.stream(st):
+            for layer in range(n_layers):
+                check(lib.tf_q_fill_synthetic(C.c_void_p(q.data_ptr()), C.c_void_p(rows.data_ptr()),
+                                              C.c_void_p(posd.data_ptr()), B, layer, hq, self.pool.D, self.seed,
+                                              C.c_void_p(st.cuda_stream)), "tf_q_fill_synthetic")
+                check(lib.tf_paged_decode_attn(self.pool.handle, C.c_void_p(q.data_ptr()),
+                                               C.c_void_p(self.table.data_ptr()), self.nlb,
+                                               C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B,
+                                               max(pos) + 1, layer, hq, scale, C.c_void_p(out.data_ptr()),
+                                               C.c_void_p(self._attn_ws.data_ptr()), self._attn_ws.numel(),
+                                               C.c_void_p(st.cuda_stream)), "tf_paged_decode_attn")
+                self.stats["attn_launches"] += 1
+        self.attn_out = (list(batch), pos, out)
+
+    # ------------------------------------------------------------ inspection
+    def synchronize(self):
+        for s in {self.s_compute, self.s_evict, self.s_load}:
+            s.synchronize()
+
+    def block_table(self, rid):
+        return self.gtab[rid].copy()
+
+    def host_table(self, rid):
+        return self.htab[rid].copy()
+
+    def device_table(self) -> np.ndarray:
+        self.synchronize()
+        return self.table.cpu().numpy()
+
+    def transfer_log(self):
+        """(direction, tokens, ms) of every launched chunk (synchronises)."""
+        self.synchronize()
+        return [(k, n, a.elapsed_time(b)) for k, n, a, b in self._events]

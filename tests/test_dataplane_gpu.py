@@ -1,0 +1,180 @@
+"""End-to-end parity of the GPU data plane in replay mode.
+
+The product runtime (engine.py) runs a golden trace with the GPU selector
+policy and the GPU data plane (block manager + swap kernels + KV append +
+paged attention).  Checks:
+  * event hash / decision log / chunk rows == the reference's (golden);
+  * every block-table and host-table transition == the CPU restatement
+    (oracle/dataplane.py) driven by the same hook calls - bit-exact;
+  * HBM pool and pinned host-store bytes of every live / host-valid token
+    == the restatement's bytes (synthetic KV), checked every few hundred
+    events and at the end of every run.
+"""
+import numpy as np
+import pytest
+from conftest import load_golden, pool_blocks, trace_path
+
+from oracle.dataplane import CpuDataPlane, attention_ref, bf16_to_f32, q_bits
+
+pytestmark = pytest.mark.gpu
+
+RUNS = ["figure7_tokenflow", "c1_tokenflow", "c1_tokenflow_no_overlap", "c1_tokenflow_no_write_through",
+        "c1_tokenflow_no_offload", "table2_s3_full", "table2_s4_no_overlap", "table2_s5_no_write_through",
+        "c1_qoe", "c1_fcfs"]
+
+
+class _OracleView:
+    """Adapter: the oracle hooks read sim.R[rid].kv / .state and sim.h2d.busy."""
+
+    def __init__(self, eng):
+        self.eng = eng
+
+    @property
+    def R(self):
+        return {rid: _St(s) for rid, s in self.eng.state.items()}
+
+    @property
+    def h2d(self):
+        return _Lane(self.eng.h2d.in_service)
+
+
+class _St:
+    def __init__(self, s):
+        self.kv, self.state = s.kv, s.status
+
+
+class _Lane:
+    def __init__(self, busy):
+        self.busy = busy
+
+
+class Tee:
+    """Forwards every hook to the GPU plane and the CPU restatement; compares."""
+
+    def __init__(self, gpu, cpu, check_every=200):
+        self.gpu, self.cpu = gpu, cpu
+        self.n = 0
+        self.check_every = check_every
+        self.byte_checks = 0
+        self.stats = gpu.stats
+
+    def _both(self, name, *args, eng=None, rids=()):
+        getattr(self.gpu, name)(*args, *(() if eng is None else (eng,)))
+        getattr(self.cpu, name)(*args, *(() if eng is None else (_OracleView(eng),)))
+        for rid in rids:
+            assert np.array_equal(self.gpu.block_table(rid), self.cpu.block_table(rid)), (name, rid)
+            assert np.array_equal(self.gpu.host_table(rid), self.cpu.host_table(rid)), (name, rid)
+
+    def fill_start(self, job, eng): self._both("fill_start", job, eng=eng, rids=job.members)
+    def fill_done(self, rid): self._both("fill_done", rid, rids=(rid,))
+    def decode_start(self, batch, eng): self._both("decode_start", batch, eng=eng, rids=batch)
+    def decode_done(self, batch, made): self._both("decode_done", batch, made, rids=batch)
+    def d2h_start(self, ch, eng): self._both("d2h_start", ch, eng=eng, rids=(ch.owner,))
+    def d2h_done(self, ch, alive): self._both("d2h_done", ch, alive, rids=(ch.owner,))
+    def h2d_start(self, ch, eng): self._both("h2d_start", ch, eng=eng, rids=(ch.owner,))
+    def release_prefix(self, rid, n): self._both("release_prefix", rid, n, rids=(rid,))
+    def cancel_evicts(self, rid): self._both("cancel_evicts", rid, rids=(rid,))
+    def drop_gpu(self, rid): self._both("drop_gpu", rid, rids=(rid,))
+    def drop_host(self, rid): self._both("drop_host", rid, rids=(rid,))
+    def finish(self, rid): self._both("finish", rid, rids=(rid,))
+
+    def synchronize(self):
+        self.gpu.synchronize()
+
+    def audit(self, eng):
+        self.gpu.audit(eng)
+        self.cpu.audit(_OracleView(eng))
+        self.n += 1
+        if self.n % self.check_every == 0:
+            self.compare_bytes(eng)
+
+    def compare_bytes(self, eng):
+        self.gpu.synchronize()
+        pool = self.gpu.pool.gpu_view().cpu().numpy().view(np.uint16)
+        host = self.gpu.pool.host_view().numpy().view(np.uint16)
+        dev_tab = self.gpu.table.cpu().numpy()
+        for rid in eng.state:
+            live = self.cpu.live_positions(rid)
+            tab = self.cpu.block_table(rid)
+            mapped = tab >= 0
+            assert np.array_equal(dev_tab[rid][mapped], tab[mapped]), f"device table row {rid}"
+            if len(live):
+                blk, slot = tab[live // 16], live % 16
+                assert np.array_equal(pool[blk, :, :, :, slot], self.cpu.pool[blk, :, :, :, slot]), f"pool {rid}"
+            hi = self.cpu.host_hi[rid]
+            if hi:
+                pos = np.arange(hi)
+                hb = self.cpu.host_table(rid)[pos // 16]
+                ok = hb >= 0
+                assert np.array_equal(host[hb[ok], :, :, :, (pos % 16)[ok]],
+                                      self.cpu.host[hb[ok], :, :, :, (pos % 16)[ok]]), f"host {rid}"
+        self.byte_checks += 1
+
+
+def _engine(name, cuda, check_every=150):
+    from paper_2510_02758_b200.costs import CostModel
+    from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
+    from paper_2510_02758_b200.engine import Engine, SimConfig
+    from paper_2510_02758_b200.scheduler import SchedulerConfig, make_policy
+    from paper_2510_02758_b200.workload import load_trace
+
+    g = load_golden("runs", name)
+    tr = load_trace(trace_path(g["trace"]))
+    nb = pool_blocks(g["sim"], len(tr.requests))
+    nh = 8192
+    pool = KvPool(nb, nh, n_layers=2, kv_heads=2, head_dim=64, device=cuda)
+    gpu = GpuDataPlane(tr.requests, pool, mode="replay", attention="all", n_q_heads=4)
+    cpu = CpuDataPlane(tr.requests, nb, nh, 2, 2, 64)
+    tee = Tee(gpu, cpu, check_every)
+    eng = Engine(tr, make_policy(g["policy"], SchedulerConfig(**g["sched"])), CostModel(**g["cm"]),
+                 SimConfig(**g["sim"]), dataplane=tee)
+    return g, eng, tee, pool
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_replay_parity(name, cuda):
+    g, eng, tee, pool = _engine(name, cuda)
+    res = eng.run()
+    assert res.event_hash() == g["event_hash"]
+    assert res.decision_log == g["decision_log"]
+    if "chunks" in g:
+        assert res.chunk_rows() == g["chunks"]
+    tee.compare_bytes(eng)
+    assert tee.byte_checks >= 2
+    st = res.stats
+    assert st["d2h_tokens"] == sum(c[2] for c in g.get("chunks", []) if c[0] == "d2h") or "chunks" not in g
+    assert st["h2d_tokens"] == sum(c[2] for c in g.get("chunks", []) if c[0] == "h2d") or "chunks" not in g
+    pool.close()
+
+
+def test_attention_inside_engine_matches_fp32(cuda):
+    """Mid-run decode attention outputs vs fp32 over the restatement's KV."""
+    g, eng, tee, pool = _engine("c1_tokenflow", cuda, check_every=10 ** 9)
+    orig = tee.decode_start
+    seen = []
+
+    def spy(batch, e):
+        orig(batch, e)
+        if len(seen) < 25 and len(seen) < (e.now * 4):
+            tee.gpu.synchronize()
+            rows, pos, out = tee.gpu.attn_out
+            seen.append((rows, pos, out.cpu().numpy().view(np.uint16).copy(),
+                         {r: tee.cpu.block_table(r) for r in rows}, tee.cpu.pool.copy()))
+
+    tee.decode_start = spy
+    eng.run()
+    assert seen
+    worst = 0.0
+    for rows, pos, out, tabs, cpool in seen:
+        for i, (rid, p) in enumerate(zip(rows, pos)):
+            t = np.arange(p + 1)
+            blk, slot = tabs[rid][t // 16], t % 16
+            layer = pool.L - 1  # the kernel's last launch is for the last layer
+            k = bf16_to_f32(cpool[blk, layer, 0, :, slot])  # [T][H][D]
+            v = bf16_to_f32(cpool[blk, layer, 1, :, slot])
+            q = bf16_to_f32(q_bits(rid, p, layer, np.arange(4)[:, None], np.arange(64)[None, :]))
+            ref = attention_ref(q, k, v, 1.0 / 8.0)
+            got = bf16_to_f32(out[i])
+            worst = max(worst, float(np.abs(got - ref).max()))
+    # bf16 output of fp32-accumulated attention: max-abs 2e-2 relative to fp32 (north star)
+    assert worst <= 2e-2, worst

@@ -1,0 +1,161 @@
+"""Kernel-level GPU tests: swap gather/scatter (both engines, Llama3-8B
+block shape, ragged token ranges, layer sub-ranges), KV append, paged decode
+attention vs an fp32 reference (GQA 32/8 hd128, 4/2 hd64, 40/8), empty and
+maximum-size cases."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    from paper_2510_02758_b200 import _lib
+
+    return _lib
+
+
+def _pool(cuda, nb, nh, L, H, D):
+    from paper_2510_02758_b200.dataplane import KvPool
+
+    p = KvPool(nb, nh, L, H, D, device=cuda)
+    g = torch.Generator(device="cpu").manual_seed(0)
+    p.gpu.copy_(torch.randint(-32768, 32767, p.gpu.shape, dtype=torch.int16, generator=g).to(cuda))
+    p.host.copy_(torch.randint(-32768, 32767, p.host.shape, dtype=torch.int16, generator=g))
+    return p
+
+
+def _segs(lib, segs):
+    arr = (lib.TfSeg * max(1, len(segs)))()
+    for i, s in enumerate(segs):
+        arr[i].gpu_block, arr[i].host_block, arr[i].slot_begin, arr[i].n_slots = s
+    return arr
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("shape", [(2, 2, 64), (32, 8, 128)])
+def test_swap_roundtrip(cuda, engine, shape):
+    L, H, D = shape
+    lib = _lib()
+    nb, nh = 48, 40
+    p = _pool(cuda, nb, nh, L, H, D)
+    rng = np.random.default_rng(engine * 7 + L)
+    segs = []
+    gb = rng.permutation(nb)[:30]
+    hb = rng.permutation(nh)[:30]
+    for i in range(30):
+        s0 = int(rng.integers(0, 16))
+        n = int(rng.integers(1, 17 - s0)) if i % 3 else 16 - (s0 := 0)
+        segs.append((int(gb[i]), int(hb[i]), s0, n))
+    for l0, l1 in ((0, L), (L // 2, L), (0, 1)):
+        before_gpu = p.gpu_view().cpu().clone()
+        before_host = p.host_view().clone()
+        st = torch.cuda.Stream()
+        lib.check(lib.lib.tf_kv_gather_d2h(p.handle, _segs(lib, segs), len(segs), l0, l1, engine,
+                                           C.c_void_p(st.cuda_stream)))
+        st.synchronize()
+        host = p.host_view()
+        exp_host = before_host.clone()
+        for g, h, s, n in segs:
+            exp_host[h, l0:l1, :, :, s:s + n] = before_gpu[g, l0:l1, :, :, s:s + n]
+        assert torch.equal(host, exp_host)
+        # scatter back into different blocks, then compare
+        segs2 = [((g + 7) % nb, h, s, n) for g, h, s, n in segs]
+        before_gpu2 = p.gpu_view().cpu().clone()
+        lib.check(lib.lib.tf_kv_scatter_h2d(p.handle, _segs(lib, segs2), len(segs2), l0, l1, engine,
+                                            C.c_void_p(st.cuda_stream)))
+        st.synchronize()
+        exp_gpu = before_gpu2.clone()
+        for g, h, s, n in segs2:
+            exp_gpu[g, l0:l1, :, :, s:s + n] = exp_host[h, l0:l1, :, :, s:s + n]
+        assert torch.equal(p.gpu_view().cpu(), exp_gpu)
+    p.close()
+
+
+def test_swap_rejects_bad_segments(cuda):
+    lib = _lib()
+    p = _pool(cuda, 4, 4, 2, 2, 64)
+    with pytest.raises(ValueError):
+        lib.check(lib.lib.tf_kv_gather_d2h(p.handle, _segs(lib, [(9, 0, 0, 4)]), 1, 0, 2, 0, None))
+    with pytest.raises(ValueError):
+        lib.check(lib.lib.tf_kv_gather_d2h(p.handle, _segs(lib, [(0, 0, 10, 8)]), 1, 0, 2, 0, None))
+    with pytest.raises(ValueError):
+        lib.check(lib.lib.tf_kv_scatter_h2d(p.handle, _segs(lib, [(0, 0, 0, 4)]), 1, 1, 1, 0, None))
+    lib.check(lib.lib.tf_kv_gather_d2h(p.handle, _segs(lib, []), 0, 0, 2, 0, None))  # empty is a no-op
+    p.close()
+
+
+def _attn_case(cuda, B, ctx_list, L, H, HQ, D, layer):
+    lib = _lib()
+    nblk_req = [(c + 15) // 16 for c in ctx_list]
+    nb = sum(nblk_req) + 3
+    p = _pool(cuda, nb, 1, L, H, D)
+    # bf16-valid random KV (randint bits could be NaN/Inf)
+    kv = (torch.randn(p.gpu.numel(), device=cuda) * 0.5).to(torch.bfloat16).view(torch.int16)
+    p.gpu.copy_(kv)
+    maxlb = max(nblk_req)
+    perm = np.random.default_rng(1).permutation(nb)
+    table = np.full((B, maxlb), -1, np.int32)
+    k = 0
+    for b in range(B):
+        table[b, : nblk_req[b]] = perm[k:k + nblk_req[b]]
+        k += nblk_req[b]
+    tab_d = torch.from_numpy(table).to(cuda)
+    rows = torch.arange(B, dtype=torch.int32, device=cuda)
+    ctx = torch.tensor(ctx_list, dtype=torch.int32, device=cuda)
+    q = (torch.randn(B, HQ, D, device=cuda)).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    ws_n = max(1, int(lib.lib.tf_paged_decode_attn_workspace(p.handle, B, max(ctx_list), HQ)))
+    ws = torch.empty(ws_n, dtype=torch.uint8, device=cuda)
+    lib.check(lib.lib.tf_paged_decode_attn(p.handle, C.c_void_p(q.data_ptr()), C.c_void_p(tab_d.data_ptr()), maxlb,
+                                           C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B, max(ctx_list),
+                                           layer, HQ, 1.0 / D ** 0.5, C.c_void_p(out.data_ptr()),
+                                           C.c_void_p(ws.data_ptr()), ws_n, None))
+    torch.cuda.synchronize()
+    pool = p.gpu_view().view(torch.bfloat16).float()
+    worst = 0.0
+    G = HQ // H
+    for b in range(B):
+        t = torch.arange(ctx_list[b], device=cuda)
+        blk = tab_d[b][(t // 16).long()].long()
+        kk = pool[blk, layer, 0, :, (t % 16).long()]  # [T][H][D]
+        vv = pool[blk, layer, 1, :, (t % 16).long()]
+        for h in range(HQ):
+            s = (kk[:, h // G, :] @ q[b, h].float()) / D ** 0.5
+            ref = torch.softmax(s.double(), 0).float() @ vv[:, h // G, :]
+            worst = max(worst, (out[b, h].float() - ref).abs().max().item())
+    p.close()
+    return worst
+
+
+@pytest.mark.parametrize("case", [
+    (8, [1, 15, 16, 17, 100, 700, 2049, 4000], 32, 8, 32, 128, 31),
+    (5, [3, 64, 200, 513, 1000], 2, 2, 4, 64, 1),
+    (3, [17, 900, 4096], 4, 8, 40, 128, 2),
+    (1, [1], 2, 2, 4, 64, 0),
+])
+def test_paged_attention_vs_fp32(cuda, case):
+    worst = _attn_case(cuda, *case)
+    assert worst <= 2e-2, worst  # bf16 output, fp32 accumulation (north-star tolerance)
+
+
+def test_kv_append_writes_slots(cuda):
+    lib = _lib()
+    L, H, D = 2, 2, 64
+    p = _pool(cuda, 8, 1, L, H, D)
+    table = torch.tensor([[3, 5], [6, -1]], dtype=torch.int32, device=cuda)
+    rows = torch.tensor([0, 0, 1], dtype=torch.int32, device=cuda)
+    pos = torch.tensor([0, 17, 9], dtype=torch.int32, device=cuda)
+    kv = torch.randint(-1000, 1000, (3, 2, H, D), dtype=torch.int16, device=cuda)
+    lib.check(lib.lib.tf_kv_append(p.handle, C.c_void_p(table.data_ptr()), 2, C.c_void_p(rows.data_ptr()),
+                                   C.c_void_p(pos.data_ptr()), 3, 1, C.c_void_p(kv[:, 0].data_ptr()),
+                                   C.c_void_p(kv[:, 1].data_ptr()), 2 * H * D, None))
+    torch.cuda.synchronize()
+    g = p.gpu_view().cpu()
+    kvc = kv.cpu()
+    for i, (blk, slot) in enumerate([(3, 0), (5, 1), (6, 9)]):
+        assert torch.equal(g[blk, 1, 0, :, slot], kvc[i, 0])
+        assert torch.equal(g[blk, 1, 1, :, slot], kvc[i, 1])
+    p.close()
