@@ -1,0 +1,95 @@
+"""CPU baseline / reference arm (TEST INFRASTRUCTURE; timed, never shipped).
+
+Times the oracle's CPU restatement of one C2 decode step on the host cores:
+  * Llama3-8B layer forward for B tokens (torch CPU, bf16 GEMMs, all threads)
+  * fp32 GQA decode attention over each member's KV (ctx tokens)
+  * KV gather of one step's swap traffic (numpy fancy-index copy)
+  * the buffer-aware tick decision (oracle.refsim.policy) on a C2 snapshot
+A bounded sample: L_SAMPLE of the 32 layers are executed and the per-layer
+cost is scaled to 32 layers (every layer does identical work); the sample
+description says so.  When the host cannot keep up with its readers every
+token is generated into an empty buffer, so its effective weight is 1 and
+effective tok/s = B / step time.
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+L_SAMPLE = 2
+
+
+def _tick_seconds(reps=3) -> float:
+    from oracle.refsim.policy import Knobs, TokenFlowPolicy, snapshot_from_dict
+
+    g = json.load(gzip.open(ROOT / "tests" / "golden" / "ticks" / "c2_burst256_s1_tokenflow.json.gz"))
+    views = [t["view"] for t in g["ticks"]][:reps]
+    t0 = time.perf_counter()
+    for v in views:
+        pol = TokenFlowPolicy(Knobs(**g["sched"]))
+        pol.on_tick(snapshot_from_dict(v))
+    return (time.perf_counter() - t0) / len(views)
+
+
+def time_cpu_step(batch: int = 64, ctx: int = 2600, threads: int = 16, seconds: float = 20.0,
+                  swap_tokens_per_step: int = 64) -> dict:
+    from paper_2510_02758_b200.configs import LLAMA3_8B as S
+
+    torch.set_num_threads(threads)
+    d, hq, hkv, hd, ffn = S.hidden, S.n_q_heads, S.n_kv_heads, S.head_dim, S.ffn
+    bf = torch.bfloat16
+    layers = [{k: torch.zeros(*sh, dtype=bf) for k, sh in (("wqkv", (d, (hq + 2 * hkv) * hd)), ("wo", (hq * hd, d)),
+                                                             ("wgu", (d, 2 * ffn)), ("wd", (ffn, d)))}
+              for _ in range(L_SAMPLE)]
+    lm = torch.zeros(d, S.vocab, dtype=bf)
+    kv = [torch.randn(batch, 2, hkv, ctx, hd, dtype=torch.float32) for _ in range(L_SAMPLE)]
+    x0 = torch.randn(batch, d, dtype=bf)
+
+    def layer_pass(li):
+        L = layers[li]
+        x = x0
+        qkv = (x @ L["wqkv"]).float().view(batch, hq + 2 * hkv, hd)
+        q = qkv[:, :hq]
+        k = kv[li][:, 0]
+        v = kv[li][:, 1]
+        qg = q.view(batch, hkv, hq // hkv, hd)
+        s = torch.einsum("bkgd,bktd->bkgt", qg, k) / hd ** 0.5
+        a = torch.einsum("bkgt,bktd->bkgd", torch.softmax(s, -1), v).reshape(batch, hq * hd).to(bf)
+        x = x + a @ L["wo"]
+        gu = x @ L["wgu"]
+        g, u = gu.chunk(2, -1)
+        return x + (torch.nn.functional.silu(g) * u) @ L["wd"]
+
+    # warm-up, then sample
+    layer_pass(0)
+    per_layer, n = [], 0
+    t_end = time.perf_counter() + seconds * 0.7
+    while time.perf_counter() < t_end or n < 2:
+        t0 = time.perf_counter()
+        layer_pass(n % L_SAMPLE)
+        per_layer.append(time.perf_counter() - t0)
+        n += 1
+    t0 = time.perf_counter()
+    (x0 @ lm).argmax(-1)
+    t_lm = time.perf_counter() - t0
+    # swap: gather one step's chunk bytes (128 KiB per token) from a pool
+    pool = np.zeros((256, 2 * 1024 * 1024 // 2), np.uint16)
+    idx = np.random.default_rng(0).permutation(256)[: max(1, swap_tokens_per_step // 16)]
+    t0 = time.perf_counter()
+    for _ in range(3):
+        pool[idx].copy()
+    t_swap = (time.perf_counter() - t0) / 3
+    t_tick = _tick_seconds()
+    ticks_per_step = 0.5 / 0.0075  # one tick per 0.5 s of schedule interval at ~7.5 ms steps
+    step = float(np.median(per_layer)) * S.n_layers + t_lm + t_swap + t_tick / ticks_per_step
+    return {"value": batch / step, "unit": "effective tok/s", "cores": threads, "kind": "port",
+            "step_s": step, "per_layer_s": float(np.median(per_layer)), "lm_head_s": t_lm, "tick_s": t_tick,
+            "sample": f"{n} single-layer passes of a B={batch}, ctx={ctx} Llama3-8B decode step (bf16 GEMMs + fp32 "
+                      f"GQA attention) scaled x{S.n_layers} layers + lm_head + one step's swap gather + 1/"
+                      f"{ticks_per_step:.0f} of an on_tick (oracle restatement); torch CPU, {threads} threads"}

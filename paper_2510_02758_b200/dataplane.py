@@ -164,19 +164,23 @@ class GpuDataPlane:
         if self.mode == "replay":
             self.pool.free(TIER_GPU, ids)
         else:
-            ev = torch.cuda.Event()
-            ev.record(self.s_compute)
-            self._quarantine.append((ev, ids))
+            # reusable once every stream has passed its current work
+            evs = []
+            for s in (self.s_compute, self.s_evict, self.s_load):
+                ev = torch.cuda.Event()
+                ev.record(s)
+                evs.append(ev)
+            self._quarantine.append((evs, ids))
 
     def _alloc_blocks(self, n):
         if self.mode == "realtime":
-            while self._quarantine and self._quarantine[0][0].query():
+            while self._quarantine and all(e.query() for e in self._quarantine[0][0]):
                 self.pool.free(TIER_GPU, self._quarantine.popleft()[1])
-            if self.pool.free_count(TIER_GPU) < n:
-                while self._quarantine and self.pool.free_count(TIER_GPU) < n:
-                    ev, ids = self._quarantine.popleft()
-                    ev.synchronize()
-                    self.pool.free(TIER_GPU, ids)
+            while self._quarantine and self.pool.free_count(TIER_GPU) < n:
+                evs, ids = self._quarantine.popleft()
+                for e in evs:
+                    e.synchronize()
+                self.pool.free(TIER_GPU, ids)
         return self.pool.alloc(TIER_GPU, n)
 
     def _flush_table(self, stream):
@@ -274,6 +278,8 @@ class GpuDataPlane:
 
     def decode_done(self, batch, made):
         made = set(made)
+        if self.model is not None and self.kv_source == "model":
+            self.model.decode_commit(made)
         for rid in batch:
             f = self.flags[rid]
             idx = np.nonzero(f & RESERVED)[0]
@@ -297,9 +303,9 @@ class GpuDataPlane:
         self.peak_host_blocks = max(self.peak_host_blocks, self.pool.n_host_blocks - self.pool.free_count(TIER_HOST))
         self.host_hi[rid] = max(self.host_hi[rid], hi)
         segs = self._segments(rid, np.arange(lo, hi))
+        # realtime: [cs, cs+n) was appended by decode steps whose completion the
+        # engine already observed, so the gather needs no wait on the compute stream
         st = self.s_evict
-        if self.mode == "realtime":
-            st.wait_stream(self.s_compute)  # positions appended by finished decodes
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(st)
@@ -313,6 +319,7 @@ class GpuDataPlane:
         self._last_d2h_event[rid] = t1
         self.stats["d2h_tokens"] += ch.tokens
         self.stats["d2h_launches"] += 1
+        return t1
 
     def d2h_done(self, ch, alive):
         rid, lo, hi, kind, ev = self._d2h_busy
@@ -346,8 +353,9 @@ class GpuDataPlane:
         self._events.append(("h2d", ch.tokens, t0, t1))
         self.stats["h2d_tokens"] += ch.tokens
         self.stats["h2d_launches"] += 1
-        if self.mode == "realtime":
-            self.s_compute.wait_event(t1)
+        # realtime: the request turns RUNNING only after the engine observed
+        # every load chunk complete, so decode needs no wait on this stream
+        return t1
 
     def release_prefix(self, rid, n):
         f = self.flags[rid]

@@ -1,0 +1,199 @@
+"""Llama-style decoder on the paged KV pool (random-init weights).
+
+Used for the C1 tiny decoder and the C2 Llama3-8B configuration.  The hot
+path ops are this package's kernels: K/V rows are appended into the paged
+block pool (tf_kv_append) and decode attention reads the block tables
+directly (tf_paged_decode_attn).  Projections / MLP / logits are plain
+cuBLAS GEMMs via torch.matmul (library GEMMs); prefill
+attention over a fresh prompt uses torch SDPA.
+
+Token pipeline (matches the reference's counts, engine.py:484-540): a
+prefill of a P-token prompt writes KV for P+1 positions - the prompt, then
+its first output token t0 at position P - and keeps t1 pending; every
+decode step emits the pending token of each member, appends its KV at
+position total_kv and computes the next pending token.  A recompute
+re-runs the prompt plus the generated tokens (positions [0, total_kv)).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+import torch.nn.functional as F
+
+from . import _lib
+from ._lib import check, lib
+
+
+class PagedDecoder:
+    def __init__(self, shape, device="cuda", seed=0, dtype=torch.bfloat16, max_batch=256):
+        self.s = shape
+        self.device = torch.device(device)
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        d, hq, hkv, hd, ffn = shape.hidden, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, shape.ffn
+
+        def w(*dims):
+            t = torch.empty(*dims, device=self.device, dtype=dtype)
+            t.normal_(0.0, 0.02, generator=g)
+            return t
+
+        self.embed = w(shape.vocab, d)
+        self.layers = []
+        for _ in range(shape.n_layers):
+            self.layers.append({
+                "ln1": torch.ones(d, device=self.device, dtype=dtype),
+                "wqkv": w(d, (hq + 2 * hkv) * hd),
+                "wo": w(hq * hd, d),
+                "ln2": torch.ones(d, device=self.device, dtype=dtype),
+                "wgu": w(d, 2 * ffn),
+                "wd": w(ffn, d),
+            })
+        self.ln_f = torch.ones(d, device=self.device, dtype=dtype)
+        self.lm_head = w(d, shape.vocab)
+        inv = 1.0 / (shape.rope_theta ** (torch.arange(0, hd, 2, device=self.device, dtype=torch.float32) / hd))
+        self._inv_freq = inv
+        self.pending = {}  # rid -> next token to emit
+        self.history = {}  # rid -> generated tokens (for recompute)
+        self.prompts = {}
+        self.scale = 1.0 / math.sqrt(hd)
+        self._ws = torch.empty(1, dtype=torch.uint8, device=self.device)
+        self.steps = 0
+        self.attn_timing = None  # list -> (algorithmic bytes, start event, end event) per attention launch
+
+    # ------------------------------------------------------------ pieces
+    def prompt_tokens(self, rid: int, n: int) -> torch.Tensor:
+        if rid not in self.prompts:
+            g = torch.Generator().manual_seed(1000003 * (rid + 1))
+            self.prompts[rid] = torch.randint(0, self.s.vocab, (n,), generator=g)
+        return self.prompts[rid]
+
+    def _rms(self, x, w):
+        return F.rms_norm(x, (x.shape[-1],), w, self.s.rms_eps)
+
+    def _rope(self, x, pos):
+        # x [n, heads, hd], pos [n] (int64)
+        ang = pos.float()[:, None] * self._inv_freq[None, :]
+        cos, sin = ang.cos()[:, None, :], ang.sin()[:, None, :]
+        x1, x2 = x[..., 0::2].float(), x[..., 1::2].float()
+        out = torch.empty_like(x)
+        out[..., 0::2] = (x1 * cos - x2 * sin).to(x.dtype)
+        out[..., 1::2] = (x1 * sin + x2 * cos).to(x.dtype)
+        return out
+
+    def _append(self, dp, rows, pos, layer, k, v, stream):
+        n = rows.numel()
+        check(lib.tf_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb, C.c_void_p(rows.data_ptr()),
+                               C.c_void_p(pos.data_ptr()), n, layer, C.c_void_p(k.data_ptr()),
+                               C.c_void_p(v.data_ptr()), k.stride(0), C.c_void_p(stream.cuda_stream)), "tf_kv_append")
+
+    def _mlp(self, x, L):
+        h = self._rms(x, L["ln2"])
+        gu = h @ L["wgu"]
+        g, u = gu.chunk(2, dim=-1)
+        return x + (F.silu(g) * u) @ L["wd"]
+
+    # ------------------------------------------------------------ forward passes
+    @torch.no_grad()
+    def _prefill_seq(self, dp, rid, tokens, pos0, stream):
+        """Causal forward of ``tokens`` at positions pos0.. (fresh sequence), writing KV."""
+        s = self.s
+        n = tokens.numel()
+        pos = torch.arange(pos0, pos0 + n, device=self.device)
+        rows = torch.full((n,), rid, dtype=torch.int32, device=self.device)
+        pos32 = pos.to(torch.int32)
+        x = self.embed[tokens.to(self.device)]
+        for li, L in enumerate(self.layers):
+            h = self._rms(x, L["ln1"])
+            qkv = (h @ L["wqkv"]).view(n, s.n_q_heads + 2 * s.n_kv_heads, s.head_dim)
+            q = self._rope(qkv[:, : s.n_q_heads], pos)
+            k = self._rope(qkv[:, s.n_q_heads: s.n_q_heads + s.n_kv_heads], pos).contiguous()
+            v = qkv[:, s.n_q_heads + s.n_kv_heads:].contiguous()
+            self._append(dp, rows, pos32, li, k.view(n, -1), v.view(n, -1), stream)
+            a = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k.transpose(0, 1)[None],
+                                               v.transpose(0, 1)[None], is_causal=True, enable_gqa=True)
+            x = x + a[0].transpose(0, 1).reshape(n, -1) @ L["wo"]
+            x = self._mlp(x, L)
+        return (self._rms(x[-1:], self.ln_f) @ self.lm_head).argmax(-1)
+
+    @torch.no_grad()
+    def prefill(self, dp, job, spans, eng):
+        st = dp.s_compute
+        with torch.cuda.stream(st):
+            for rid, lo, hi in spans:
+                spec = eng.state[rid].spec
+                if job.kind == "recompute":
+                    toks = torch.cat([self.prompt_tokens(rid, spec.prompt_len),
+                                      torch.tensor(self.history.get(rid, []), dtype=torch.long)])[: hi - lo]
+                    self._prefill_seq(dp, rid, toks, 0, st)
+                    continue
+                if job.kind == "chunk" and not job.emits_first_token:
+                    toks = self.prompt_tokens(rid, spec.prompt_len)[lo:hi]
+                    self._prefill_seq(dp, rid, toks, lo, st)  # chunked prefill (baseline policy)
+                    continue
+                prompt = self.prompt_tokens(rid, spec.prompt_len)
+                t0 = self._prefill_seq(dp, rid, prompt[lo:], lo, st) if hi - 1 > lo else prompt[-1:].to(self.device)
+                t1 = self._decode_rows(dp, [rid], t0.view(1), [hi - 1], st)
+                self.history[rid] = [int(t0.item())]
+                self.pending[rid] = int(t1[0].item())
+
+    @torch.no_grad()
+    def decode(self, dp, batch, eng):
+        st = dp.s_compute
+        pos = [eng.state[r].kv.total_kv for r in batch]
+        with torch.cuda.stream(st):
+            toks = torch.tensor([self.pending[r] for r in batch], dtype=torch.long).pin_memory()
+            nxt = self._decode_rows(dp, list(batch), toks.to(self.device, non_blocking=True), pos, st)
+            self._last = (list(batch), nxt)
+        self.steps += 1
+
+    def decode_commit(self, made):
+        """Host side of a finished decode step: emit pending tokens of members that produced."""
+        batch, nxt = self._last
+        host = nxt.cpu().tolist()
+        for rid, t in zip(batch, host):
+            if rid in made:
+                self.history.setdefault(rid, []).append(self.pending[rid])
+                self.pending[rid] = t
+
+    def _decode_rows(self, dp, rids, tokens, positions, st):
+        s = self.s
+        B = len(rids)
+        rows = torch.tensor(rids, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        pos32 = torch.tensor(positions, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        ctx = pos32 + 1
+        pos = pos32.long()
+        max_ctx = max(positions) + 1
+        need = int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, s.n_q_heads))
+        if need > self._ws.numel():
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        x = self.embed[tokens]
+        attn = torch.empty((B, s.n_q_heads, s.head_dim), device=self.device, dtype=x.dtype)
+        timing = self.attn_timing
+        if timing is not None:
+            # algorithmic bytes of one launch: K+V of every context token, q in,
+            # out, block-table entries
+            abytes = (sum(positions) + B) * 2 * s.n_kv_heads * s.head_dim * 2 + 2 * B * s.n_q_heads * s.head_dim * 2 \
+                + sum((p + 16) // 16 for p in positions) * 4
+        for li, L in enumerate(self.layers):
+            h = self._rms(x, L["ln1"])
+            qkv = (h @ L["wqkv"]).view(B, s.n_q_heads + 2 * s.n_kv_heads, s.head_dim)
+            q = self._rope(qkv[:, : s.n_q_heads], pos).contiguous()
+            k = self._rope(qkv[:, s.n_q_heads: s.n_q_heads + s.n_kv_heads], pos).contiguous()
+            v = qkv[:, s.n_q_heads + s.n_kv_heads:].contiguous()
+            self._append(dp, rows, pos32, li, k.view(B, -1), v.view(B, -1), st)
+            if timing is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+            check(lib.tf_paged_decode_attn(dp.pool.handle, C.c_void_p(q.data_ptr()), C.c_void_p(dp.table.data_ptr()),
+                                           dp.nlb, C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B, max_ctx,
+                                           li, s.n_q_heads, self.scale, C.c_void_p(attn.data_ptr()),
+                                           C.c_void_p(self._ws.data_ptr()), self._ws.numel(),
+                                           C.c_void_p(st.cuda_stream)), "tf_paged_decode_attn")
+            if timing is not None:
+                e1.record(st)
+                timing.append((abytes, e0, e1))
+            dp.stats["attn_launches"] += 1
+            x = x + attn.view(B, -1) @ L["wo"]
+            x = self._mlp(x, L)
+        return (self._rms(x, self.ln_f) @ self.lm_head).argmax(-1)

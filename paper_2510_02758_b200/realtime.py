@@ -1,0 +1,226 @@
+"""Real-time serving loop over the GPU data plane (measured clock).
+
+Same handlers and policy as the replay engine (engine.py), but time is the
+wall clock and every duration comes from the hardware:
+
+* a decode iteration / prefill is launched on the compute stream and
+  completes when its CUDA end event fires; the engine time of completion is
+  the event's device timestamp (cudaEventElapsedTime from an anchor event),
+  so the reported ``iter_time`` is the kernels' real duration;
+* write-through / evict chunks run on the evict stream and loads on the
+  load stream concurrently with decode (the reference's full-duplex PCIe
+  pair, engine.py:235-247); their measured token rates feed
+  ``update_rate_ema`` exactly like the reference's simulated ones;
+* readers consume on the same clock at their configured rates.
+
+``skip_idle``: when the GPU and both copy streams are idle and the next
+event is a reader / arrival / tick in the future, the clock jumps to it
+instead of sleeping (nothing is in flight, so no measured duration spans a
+jump).  Busy periods run at true wall-clock speed, so copy/compute overlap
+is real; only idle gaps are compressed.  A run therefore takes about the
+GPU's busy time instead of the readers' reading time.
+"""
+from __future__ import annotations
+
+import heapq
+import time
+
+import torch
+
+from .engine import (
+    CHUNK_TRANSFER_DONE,
+    DECODE_ITER_DONE,
+    PREFILL_DONE,
+    PREFILL_WAIT,
+    PREFILLING,
+    DeadlockError,
+    Engine,
+    _Job,
+)
+
+
+class RealtimeEngine(Engine):
+    def __init__(self, trace, policy, cm, sim, dataplane, skip_idle: bool = True, on_step=None, max_steps=None):
+        super().__init__(trace, policy, cm, sim, dataplane)
+        assert dataplane is not None and dataplane.mode == "realtime"
+        self.skip_idle = skip_idle
+        self.on_step = on_step  # callback(record dict) after every decode iteration
+        self.max_steps = max_steps
+        self.steps = []  # per decode iteration: start, end, batch size, produced, effective weight
+        self._gpu = None  # (kind, payload, start_time, end_event)
+        self._lanes = {"d2h": None, "h2d": None}  # (start_time, end_event)
+        self._anchor = None
+        self.skipped_s = 0.0
+        self.wall_s = 0.0
+        self._stop = False
+
+    # ------------------------------------------------------------------ clock
+    def _clock(self) -> float:
+        return time.perf_counter() - self._t0 + self.skipped_s
+
+    def _reanchor(self):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(self.dp.s_compute)
+        ev.synchronize()
+        self._anchor = (ev, self._clock())
+
+    def _event_time(self, ev) -> float:
+        a, t = self._anchor
+        return t + a.elapsed_time(ev) / 1e3
+
+    # ------------------------------------------------------------ dispatching
+    def _dispatch_gpu(self, time_):
+        if self.gpu_job is not None:
+            return
+        start = time_
+        prefer_decode = (self.policy.interleave_prefill_chunks and self._last_gpu_kind == "prefill"
+                         and bool(self._decode_candidates()))
+        if self.prefill_queue and not prefer_decode:
+            job = self.prefill_queue[0]
+            need = sum(job.reserve.values())
+            if need <= self._mem_free():
+                self.prefill_queue.popleft()
+                for rid in job.members:
+                    self._uncommit(rid, job.reserve[rid])
+                    if self.state[rid].status == PREFILL_WAIT:
+                        self.state[rid].status = PREFILLING
+                self._mem_acquire(need)
+                self.dp.fill_start(job, self)
+                self.gpu_job = job
+                self._gpu = ("prefill", job, start, self._end_event())
+                return
+        chosen = self._decode_candidates()
+        if not chosen:
+            return
+        free = max(0, self._growth_budget())
+        if len(chosen) > free:
+            chosen = self._shed_for_memory(time_, chosen, free)
+        if not chosen:
+            return
+        batch = tuple(chosen)
+        self.dp.decode_start(batch, self)
+        self.gpu_job = ("decode", batch)
+        self._gpu = ("decode", batch, start, self._end_event())
+
+    def _end_event(self):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(self.dp.s_compute)
+        return ev
+
+    def _start_channel(self, time_, ch_):
+        if ch_.in_service is not None or not ch_.queue:
+            return
+        head = ch_.queue[0]
+        if ch_.direction == "h2d":
+            if not self.sim.overlap and self.d2h.carries("evict"):
+                return
+            if head.tokens > self._mem_free() - self.mem_committed:
+                return
+            self._mem_acquire(head.tokens)
+        ch_.queue.popleft()
+        ch_.in_service = head
+        ch_.started = time_
+        ev = (self.dp.d2h_start if ch_.direction == "d2h" else self.dp.h2d_start)(head, self)
+        self._lanes[ch_.direction] = (time_, ev)
+
+    # ------------------------------------------------------------------- loop
+    def _poll_completions(self) -> bool:
+        done = []
+        if self._gpu is not None and self._gpu[3].query():
+            done.append((self._event_time(self._gpu[3]), 0, "gpu"))
+        for d, v in self._lanes.items():
+            if v is not None and v[1].query():
+                done.append((max(self._event_time(v[1]), v[0]), 1, d))
+        if not done:
+            return False
+        done.sort()
+        for t, _, what in done:
+            self.now = max(self.now, t)
+            if what == "gpu":
+                kind, payload, start, _ = self._gpu
+                self._gpu = None
+                dur = max(t - start, 1e-9)
+                if kind == "prefill":
+                    self._on_prefill_done(t, min(payload.members), payload, dur)
+                else:
+                    n_before = len(self.steps)
+                    self._record_step(payload, start, t, dur)
+                    self._on_decode_iter_done(t, min(payload), payload, dur)
+                    self._finish_step(n_before)
+            else:
+                self._lanes[what] = None
+                self._on_chunk_transfer_done(t, -1, what)
+        return True
+
+    def _record_step(self, batch, start, end, dur):
+        self._step_pre = {r: (self.state[r].status, self.state[r].generated) for r in batch}
+        self.steps.append({"start": start, "end": end, "dur": dur, "batch": len(batch)})
+
+    def _finish_step(self, idx):
+        rec = self.steps[idx]
+        made, eff = 0, 0.0
+        for rid, (_, g0) in self._step_pre.items():
+            st = self.state[rid]
+            if st.generated > g0:
+                made += 1
+                b = st.record.buffer_at_gen[-1]
+                lo, hi = 0.10 * st.spec.output_len, 0.20 * st.spec.output_len
+                eff += 1.0 if b < lo else (0.0 if b >= hi else (hi - b) / (hi - lo))
+        rec["tokens"], rec["effective"] = made, eff
+        if self.on_step is not None:
+            self.on_step(rec, self)
+        if self.max_steps is not None and len(self.steps) >= self.max_steps:
+            self._stop = True
+
+    def run(self):
+        for r in self.trace.requests:
+            self._push(r.arrival_time, "arrival", r.id)
+        self._push(0.0, "schedule_tick", -1)
+        handlers = {"arrival": self._on_arrival, "schedule_tick": self._on_schedule_tick,
+                    "request_done": self._on_request_done, "consume": self._on_consume}
+        self._t0 = time.perf_counter()
+        self._reanchor()
+        wall0 = time.perf_counter()
+        idle_spins = 0
+        while self.live > 0 and not self._stop:
+            progressed = self._poll_completions()
+            now = self._clock()
+            while self._heap and self._heap[0][0] <= now:
+                t, _, subject, seq = heapq.heappop(self._heap)
+                kind, payload = self._payload.pop(seq)
+                self.now = max(self.now, t)
+                self._last_event_time = self.now
+                handlers[kind](t, subject, *payload)
+                progressed = True
+                if self.live == 0 or self._stop:
+                    break
+            if progressed:
+                idle_spins = 0
+                continue
+            busy = self._gpu is not None or any(v is not None for v in self._lanes.values())
+            if not busy:
+                if not self._heap:
+                    raise DeadlockError(f"{self.live} requests incomplete but nothing is scheduled")
+                gap = self._heap[0][0] - self._clock()
+                if gap > 0:
+                    if self.skip_idle:
+                        self.skipped_s += gap
+                        self._reanchor()
+                    else:
+                        time.sleep(min(gap, 0.01))
+            else:
+                idle_spins += 1
+                if idle_spins > 64:
+                    time.sleep(20e-6)
+        self.dp.synchronize()
+        self.wall_s = time.perf_counter() - wall0
+        self._last_event_time = max(self._last_event_time, self.now)
+        return self._result()
+
+    def _result(self):
+        from .engine import SimResult
+
+        records = [self.state[r.id].record for r in self.trace.requests]
+        return SimResult(self.policy.name, records, self.event_log, self.decision_log, self._last_event_time,
+                         self.total_preemptions, self.total_recomputes,
+                         list(getattr(self.policy, "mode_changes", [])), dict(self.dp.stats))
