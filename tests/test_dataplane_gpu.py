@@ -96,6 +96,7 @@ class Tee:
             self.compare_bytes(eng)
 
     def compare_bytes(self, eng):
+        self.gpu._flush_table(self.gpu.s_compute)  # table deltas are applied lazily before the next kernel
         self.gpu.synchronize()
         pool = self.gpu.pool.gpu_view().cpu().numpy().view(np.uint16)
         host = self.gpu.pool.host_view().numpy().view(np.uint16)
