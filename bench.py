@@ -164,10 +164,16 @@ def run_ours(args):
     sim = c2.sim_cfg(SimConfig, debug_checks=False)
     cm = c2.cost_model(CostModel)
 
+    t_start = time.perf_counter()
     state = {"phase": "ff", "t_warm": None, "timed": [], "wall0": None, "wall1": None, "attn": []}
 
     def on_step(rec, eng):
         contended = eng.total_preemptions > 0
+        if args.verbose and len(eng.steps) % 200 == 0:
+            print(f"[bench] step {len(eng.steps)} t={eng.now:.2f}s batch={rec['batch']} dur={rec['dur'] * 1e3:.2f}ms "
+                  f"pre={eng.total_preemptions} rc={eng.total_recomputes} running={len(eng.running)} "
+                  f"waiting={len(eng.waiting)} d2h={dp.stats['d2h_tokens']} h2d={dp.stats['h2d_tokens']} "
+                  f"wall={time.perf_counter() - t_start:.1f}s", file=sys.stderr, flush=True)
         if state["phase"] == "ff":
             if contended or len(eng.steps) >= args.ff_max:
                 state["phase"] = "warm"
@@ -328,6 +334,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-batch", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -1,0 +1,211 @@
+"""C5: KV swap bandwidth sweep + transfer-hidden-under-decode measurement.
+
+python bench_swap.py [--max-blocks 65536] [--engines 0,1] [--out gpurun_out/swap_sweep.json]
+
+Llama3-8B block format (2 MiB per block = 16 tokens x 32 layers x K,V x 8
+heads x 128 x bf16).  For block counts 1, 2, 4, ..., max: a random
+permutation of pool block ids (seed 0) is gathered to (d2h) / scattered from
+(h2d) pinned host blocks, either all 32 layers per launch or one layer per
+launch (per-layer chunking), with the SM zero-copy kernel (engine 0) and the
+copy-engine batch path (engine 1); plus both directions concurrently on two
+streams.  GB/s are reported against PCIe Gen5 x16 (63.0 GB/s per direction)
+and against the box's measured contiguous pinned cudaMemcpyAsync peak.
+
+--overlap: decode attention over a C2-sized batch alone, swaps alone, and
+both concurrently -> hidden = 1 - (T_both - T_decode) / T_swap.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2510_02758_b200 import _lib  # noqa: E402
+from paper_2510_02758_b200.dataplane import KvPool  # noqa: E402
+
+PCIE = 63.0
+
+
+def segs_for(gblocks, hblocks):
+    arr = (_lib.TfSeg * len(gblocks))()
+    for i, (g, h) in enumerate(zip(gblocks, hblocks)):
+        arr[i].gpu_block, arr[i].host_block, arr[i].slot_begin, arr[i].n_slots = int(g), int(h), 0, 16
+    return arr
+
+
+def timed(fn, stream, reps=3):
+    fn()
+    stream.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
+def memcpy_peak(pool, stream):
+    n = min(pool.n_host_blocks, 512) * pool.block_bytes // 2
+    g, h = pool.gpu[:n], pool.host[:n]
+    d2h = timed(lambda: h.copy_(g, non_blocking=True), stream)
+    h2d = timed(lambda: g.copy_(h, non_blocking=True), stream)
+    return n * 2 / d2h / 1e9, n * 2 / h2d / 1e9
+
+
+def sweep(args):
+    dev = torch.device("cuda")
+    L, H, D = 32, 8, 128
+    pool = KvPool(args.max_blocks, args.host_blocks, L, H, D, device=dev)
+    pool.gpu.zero_()
+    bb = pool.block_bytes
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    peak_d2h, peak_h2d = memcpy_peak(pool, s1)
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(args.max_blocks)
+    rows = []
+    n = 1
+    while n <= args.max_blocks:
+        g = perm[:n]
+        h = np.arange(n) % args.host_blocks
+        segs = segs_for(g, h)
+        for eng in args.engines:
+            for per_layer in (False, True):
+                ranges = [(l, l + 1) for l in range(L)] if per_layer else [(0, L)]
+
+                def d2h(st=s1):
+                    for l0, l1 in ranges:
+                        _lib.check(_lib.lib.tf_kv_gather_d2h(pool.handle, segs, n, l0, l1, eng,
+                                                             C.c_void_p(st.cuda_stream)))
+
+                def h2d(st=s1):
+                    for l0, l1 in ranges:
+                        _lib.check(_lib.lib.tf_kv_scatter_h2d(pool.handle, segs, n, l0, l1, eng,
+                                                              C.c_void_p(st.cuda_stream)))
+
+                reps = 3 if n >= 64 else 10
+                td = timed(d2h, s1, reps)
+                th = timed(h2d, s1, reps)
+                # both directions concurrently (full duplex)
+                t0 = time.perf_counter()
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(s1)
+                s2.wait_event(e0)
+                for _ in range(reps):
+                    d2h(s1)
+                    h2d(s2)
+                e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e1.record(s1)
+                e2.record(s2)
+                torch.cuda.synchronize()
+                tb = max(e0.elapsed_time(e1), e0.elapsed_time(e2)) / 1e3 / reps
+                del t0
+                nbytes = n * bb
+                rows.append({"blocks": n, "engine": "sm" if eng == 0 else "ce", "per_layer": per_layer,
+                             "bytes": nbytes, "d2h_gbs": nbytes / td / 1e9, "h2d_gbs": nbytes / th / 1e9,
+                             "duplex_gbs": 2 * nbytes / tb / 1e9,
+                             "d2h_frac_pcie": nbytes / td / 1e9 / PCIE, "h2d_frac_pcie": nbytes / th / 1e9 / PCIE,
+                             "d2h_frac_memcpy": nbytes / td / 1e9 / peak_d2h,
+                             "h2d_frac_memcpy": nbytes / th / 1e9 / peak_h2d})
+                print(json.dumps(rows[-1]), flush=True)
+        n *= 2
+    # bit-exact round trip at the largest size, SM engine
+    k = min(args.max_blocks, args.host_blocks)
+    g = perm[:k]
+    pool.gpu.view(args.max_blocks, -1)[torch.from_numpy(g).to(dev)] = torch.randint(
+        -30000, 30000, (k, pool.block_elems), dtype=torch.int16, device=dev)
+    ref = pool.gpu.view(args.max_blocks, -1)[torch.from_numpy(g).to(dev)].clone()
+    segs = segs_for(g, np.arange(k))
+    _lib.check(_lib.lib.tf_kv_gather_d2h(pool.handle, segs, k, 0, L, 0, C.c_void_p(s1.cuda_stream)))
+    pool.gpu.view(args.max_blocks, -1)[torch.from_numpy(g).to(dev)] = 0
+    _lib.check(_lib.lib.tf_kv_scatter_h2d(pool.handle, segs, k, 0, L, 0, C.c_void_p(s1.cuda_stream)))
+    s1.synchronize()
+    ok = torch.equal(pool.gpu.view(args.max_blocks, -1)[torch.from_numpy(g).to(dev)], ref)
+    out = {"pcie_gen5_gbs": PCIE, "memcpy_peak_d2h_gbs": peak_d2h, "memcpy_peak_h2d_gbs": peak_h2d,
+           "roundtrip_bit_exact_blocks": k if ok else -1, "rows": rows}
+    if args.overlap:
+        out["overlap"] = overlap(pool, args)
+    Path(args.out).parent.mkdir(parents=True, exist_ok=True)
+    Path(args.out).write_text(json.dumps(out, indent=1))
+    print(json.dumps({k: v for k, v in out.items() if k != "rows"}))
+    pool.close()
+
+
+def overlap(pool, args):
+    """Decode attention (B=64, ctx 2600, 32 layers) alone / swaps alone / both."""
+    dev = pool.device
+    B, ctx, L, HQ = 64, 2600, 32, 32
+    nblk = (ctx + 15) // 16
+    table = torch.arange(B * nblk, dtype=torch.int32, device=dev).view(B, nblk) % (pool.n_blocks // 2)
+    rows = torch.arange(B, dtype=torch.int32, device=dev)
+    ctxs = torch.full((B,), ctx, dtype=torch.int32, device=dev)
+    q = torch.randn(B, HQ, 128, device=dev).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    ws_n = max(1, int(_lib.lib.tf_paged_decode_attn_workspace(pool.handle, B, ctx, HQ)))
+    ws = torch.empty(ws_n, dtype=torch.uint8, device=dev)
+    sc, sd, sh = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    # swap traffic of one step: 256 blocks out (write-through + evict) and 256 in (loads)
+    g = np.arange(pool.n_blocks // 2, pool.n_blocks // 2 + 256)
+    segs = segs_for(g, np.arange(256) % pool.n_host_blocks)
+    res = {}
+    for eng in args.engines:
+        def decode():
+            for layer in range(L):
+                _lib.check(_lib.lib.tf_paged_decode_attn(pool.handle, C.c_void_p(q.data_ptr()),
+                                                         C.c_void_p(table.data_ptr()), nblk,
+                                                         C.c_void_p(rows.data_ptr()), C.c_void_p(ctxs.data_ptr()),
+                                                         B, ctx, layer, HQ, 0.088, C.c_void_p(out.data_ptr()),
+                                                         C.c_void_p(ws.data_ptr()), ws_n,
+                                                         C.c_void_p(sc.cuda_stream)))
+
+        def swaps():
+            _lib.check(_lib.lib.tf_kv_gather_d2h(pool.handle, segs, 256, 0, 32, eng, C.c_void_p(sd.cuda_stream)))
+            _lib.check(_lib.lib.tf_kv_scatter_h2d(pool.handle, segs, 256, 0, 32, eng, C.c_void_p(sh.cuda_stream)))
+
+        def run(fns, reps=5):
+            for f in fns:
+                f()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                for f in fns:
+                    f()
+            torch.cuda.synchronize()
+            return (time.perf_counter() - t0) / reps
+
+        t_dec = run([decode])
+        t_swp = run([swaps])
+        t_both = run([decode, swaps])
+        hidden = 1.0 - max(0.0, t_both - t_dec) / t_swp
+        res["sm" if eng == 0 else "ce"] = {"t_decode_ms": t_dec * 1e3, "t_swap_ms": t_swp * 1e3,
+                                           "t_both_ms": t_both * 1e3, "hidden_frac": hidden,
+                                           "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = 32 layers of "
+                                                   "paged attention B=64 ctx=2600; swap = 512 MiB out + 512 MiB in"}
+        print(json.dumps(res), flush=True)
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--max-blocks", type=int, default=65536)
+    ap.add_argument("--host-blocks", type=int, default=8192)
+    ap.add_argument("--engines", default="0,1")
+    ap.add_argument("--overlap", action="store_true")
+    ap.add_argument("--out", default="gpurun_out/swap_sweep.json")
+    args = ap.parse_args()
+    args.engines = [int(x) for x in args.engines.split(",")]
+    sweep(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -30,6 +30,48 @@ __global__ void append_kernel(PoolView pv, const int32_t* __restrict__ table, in
     *reinterpret_cast<uint4*>(dst + d) = *reinterpret_cast<const uint4*>(src + d);
 }
 
+// Fused decode epilogue of the QKV projection: rotary embedding of q and k
+// (interleaved pairs, angle = pos * inv_freq[i]) + append of k, v into the
+// paged pool + q written contiguously for the attention kernel.  One warp per
+// (token, head) of the fused [hq + 2*hkv] head axis.
+__global__ void rope_append_kernel(PoolView pv, const int32_t* __restrict__ table, int32_t stride,
+                                   const int32_t* __restrict__ rows, const int32_t* __restrict__ pos, int32_t n,
+                                   int32_t layer, const uint16_t* __restrict__ qkv, int32_t hq,
+                                   const float* __restrict__ inv_freq, uint16_t* __restrict__ q_out) {
+  const int heads = hq + 2 * pv.kv_heads;
+  const int warps = blockDim.x / 32;
+  const int64_t wid = (int64_t)blockIdx.x * warps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (wid >= (int64_t)n * heads) return;
+  const int tok = (int)(wid / heads), h = (int)(wid % heads);
+  const int D = pv.head_dim;
+  const int p = pos[tok];
+  const uint16_t* src = qkv + ((int64_t)tok * heads + h) * D;
+  uint16_t* dst;
+  bool rotate = true;
+  if (h < hq) {
+    dst = q_out + ((int64_t)tok * hq + h) * D;
+  } else {
+    const int kvh = (h - hq) % pv.kv_heads, kv = (h - hq) / pv.kv_heads;
+    const int blk = table[(int64_t)rows[tok] * stride + p / pv.block_tokens];
+    dst = pv.gpu + pv.off(blk, layer, kv, kvh, p % pv.block_tokens);
+    rotate = (kv == 0);
+  }
+  for (int i = lane; i < D / 2; i += 32) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 2 * i);
+    if (!rotate) {
+      *reinterpret_cast<uint32_t*>(dst + 2 * i) = w;
+      continue;
+    }
+    const float x1 = __uint_as_float(w << 16), x2 = __uint_as_float(w & 0xFFFF0000u);
+    float sn, cs;
+    sincosf((float)p * inv_freq[i], &sn, &cs);
+    const uint32_t o1 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * cs - x2 * sn));
+    const uint32_t o2 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * sn + x2 * cs));
+    *reinterpret_cast<uint32_t*>(dst + 2 * i) = o1 | (o2 << 16);
+  }
+}
+
 constexpr int kMaxSpans = 1536;
 struct SpanArgs {
   int32_t n;
@@ -93,6 +135,23 @@ int tf_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride, con
   append_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
       view_of(*p), dev_table, row_stride, dev_rows, dev_pos, n, layer, (const uint16_t*)k, (const uint16_t*)v,
       kv_row_stride);
+  TF_LAUNCH_CHECK();
+  return TF_OK;
+}
+
+int tf_rope_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride, const int32_t* dev_rows,
+                      const int32_t* dev_pos, int32_t n, int32_t layer, const void* qkv, int32_t n_q_heads,
+                      const float* inv_freq, void* q_out, void* stream) {
+  Pool* p = get_pool(pool);
+  TF_CHECK_ARG(p, "tf_rope_kv_append: unknown pool");
+  TF_CHECK_ARG(layer >= 0 && layer < p->n_layers, "tf_rope_kv_append: bad layer %d", layer);
+  TF_CHECK_ARG(n >= 0, "tf_rope_kv_append: n < 0");
+  if (n == 0) return TF_OK;
+  TF_CHECK_ARG(dev_table && dev_rows && dev_pos && qkv && inv_freq && q_out, "tf_rope_kv_append: NULL pointer");
+  const int64_t warps = (int64_t)n * (n_q_heads + 2 * p->kv_heads);
+  rope_append_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      view_of(*p), dev_table, row_stride, dev_rows, dev_pos, n, layer, (const uint16_t*)qkv, n_q_heads, inv_freq,
+      (uint16_t*)q_out);
   TF_LAUNCH_CHECK();
   return TF_OK;
 }

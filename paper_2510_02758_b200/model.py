@@ -91,7 +91,7 @@ class PagedDecoder:
         h = self._rms(x, L["ln2"])
         gu = h @ L["wgu"]
         g, u = gu.chunk(2, dim=-1)
-        return x + (F.silu(g) * u) @ L["wd"]
+        return torch.addmm(x, F.silu(g) * u, L["wd"])
 
     # ------------------------------------------------------------ forward passes
     @torch.no_grad()
@@ -175,13 +175,15 @@ class PagedDecoder:
             # out, block-table entries
             abytes = (sum(positions) + B) * 2 * s.n_kv_heads * s.head_dim * 2 + 2 * B * s.n_q_heads * s.head_dim * 2 \
                 + sum((p + 16) // 16 for p in positions) * 4
+        q = torch.empty((B, s.n_q_heads, s.head_dim), device=self.device, dtype=x.dtype)
         for li, L in enumerate(self.layers):
             h = self._rms(x, L["ln1"])
-            qkv = (h @ L["wqkv"]).view(B, s.n_q_heads + 2 * s.n_kv_heads, s.head_dim)
-            q = self._rope(qkv[:, : s.n_q_heads], pos).contiguous()
-            k = self._rope(qkv[:, s.n_q_heads: s.n_q_heads + s.n_kv_heads], pos).contiguous()
-            v = qkv[:, s.n_q_heads + s.n_kv_heads:].contiguous()
-            self._append(dp, rows, pos32, li, k.view(B, -1), v.view(B, -1), st)
+            qkv = h @ L["wqkv"]
+            # fused rotary embedding + paged K/V append + q layout (one launch)
+            check(lib.tf_rope_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb,
+                                        C.c_void_p(rows.data_ptr()), C.c_void_p(pos32.data_ptr()), B, li,
+                                        C.c_void_p(qkv.data_ptr()), s.n_q_heads, C.c_void_p(self._inv_freq.data_ptr()),
+                                        C.c_void_p(q.data_ptr()), C.c_void_p(st.cuda_stream)), "tf_rope_kv_append")
             if timing is not None:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)
@@ -194,6 +196,6 @@ class PagedDecoder:
                 e1.record(st)
                 timing.append((abytes, e0, e1))
             dp.stats["attn_launches"] += 1
-            x = x + attn.view(B, -1) @ L["wo"]
+            x = torch.addmm(x, attn.view(B, -1), L["wo"])
             x = self._mlp(x, L)
         return (self._rms(x, self.ln_f) @ self.lm_head).argmax(-1)
