@@ -23,9 +23,10 @@ are relative to /root/reference/pkg/src):
                   block tables, token-range residency, byte movement between
                   a CPU "HBM pool" and a CPU "host store", synthetic KV
                   contents, and fp32 paged decode attention.
-* ``csrc/``     - a plain-C restatement of the selector arithmetic (glibc
-                  ``exp`` is the reference's own, so the C port reproduces
-                  ``math.exp`` exactly) used for the CPU baseline timing.
+* ``cpu_baseline`` - the CPU restatement of one C2 decode step (model
+                  forward, fp32 attention, swap gather, on_tick), timed on
+                  the host cores for bench.py's ``cpu_baseline`` and
+                  ``--impl reference`` legs.
 
 Parity pin: decisions/schedules are pinned by the reference's own outputs
 (golden fixtures).  Block tables, swapped bytes and attention are pinned by

@@ -186,8 +186,12 @@ class GpuDataPlane:
     def _flush_table(self, stream):
         if not self._pending_table:
             return
-        t = np.asarray(self._pending_table, np.int32).reshape(-1)
+        # last write per (row, lb) wins: the kernel applies triples in parallel
+        last = {}
+        for row, lb, blk in self._pending_table:
+            last[(row, lb)] = blk
         self._pending_table = []
+        t = np.asarray([(r, j, b) for (r, j), b in last.items()], np.int32).reshape(-1)
         check(lib.tf_table_apply(C.c_void_p(self.table.data_ptr()), self.nlb, _i32(t), len(t) // 3,
                                  C.c_void_p(stream.cuda_stream)), "tf_table_apply")
 
