@@ -329,7 +329,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--host-blocks", type=int, default=int(os.environ.get("TF_HOST_BLOCKS", 26000)))
-    ap.add_argument("--swap-engine", type=int, default=0)
+    ap.add_argument("--swap-engine", type=int, default=1)
     ap.add_argument("--ff-max", type=int, default=6000)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-batch", type=int, default=64)

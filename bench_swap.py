@@ -57,8 +57,11 @@ def timed(fn, stream, reps=3):
 def memcpy_peak(pool, stream):
     n = min(pool.n_host_blocks, 512) * pool.block_bytes // 2
     g, h = pool.gpu[:n], pool.host[:n]
-    d2h = timed(lambda: h.copy_(g, non_blocking=True), stream)
-    h2d = timed(lambda: g.copy_(h, non_blocking=True), stream)
+    def cp(dst, src):
+        with torch.cuda.stream(stream):
+            dst.copy_(src, non_blocking=True)
+    d2h = timed(lambda: cp(h, g), stream)
+    h2d = timed(lambda: cp(g, h), stream)
     return n * 2 / d2h / 1e9, n * 2 / h2d / 1e9
 
 
@@ -125,9 +128,12 @@ def sweep(args):
     pool.gpu.view(args.max_blocks, -1)[torch.from_numpy(g).to(dev)] = torch.randint(
         -30000, 30000, (k, pool.block_elems), dtype=torch.int16, device=dev)
     ref = pool.gpu.view(args.max_blocks, -1)[torch.from_numpy(g).to(dev)].clone()
+    torch.cuda.synchronize()  # fills above ran on the default stream
     segs = segs_for(g, np.arange(k))
     _lib.check(_lib.lib.tf_kv_gather_d2h(pool.handle, segs, k, 0, L, 0, C.c_void_p(s1.cuda_stream)))
+    s1.synchronize()
     pool.gpu.view(args.max_blocks, -1)[torch.from_numpy(g).to(dev)] = 0
+    torch.cuda.synchronize()
     _lib.check(_lib.lib.tf_kv_scatter_h2d(pool.handle, segs, k, 0, L, 0, C.c_void_p(s1.cuda_stream)))
     s1.synchronize()
     ok = torch.equal(pool.gpu.view(args.max_blocks, -1)[torch.from_numpy(g).to(dev)], ref)
@@ -154,9 +160,11 @@ def overlap(pool, args):
     ws_n = max(1, int(_lib.lib.tf_paged_decode_attn_workspace(pool.handle, B, ctx, HQ)))
     ws = torch.empty(ws_n, dtype=torch.uint8, device=dev)
     sc, sd, sh = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    # swap traffic of one step: 256 blocks out (write-through + evict) and 256 in (loads)
-    g = np.arange(pool.n_blocks // 2, pool.n_blocks // 2 + 256)
-    segs = segs_for(g, np.arange(256) % pool.n_host_blocks)
+    # swap traffic smaller than one decode's time (so 100% hiding is possible):
+    # NB blocks out (write-through + evict) and NB in (loads), 2 MiB each
+    nbk = args.overlap_blocks
+    g = np.arange(pool.n_blocks // 2, pool.n_blocks // 2 + nbk)
+    segs = segs_for(g, np.arange(nbk) % pool.n_host_blocks)
     res = {}
     for eng in args.engines:
         def decode():
@@ -169,8 +177,8 @@ def overlap(pool, args):
                                                          C.c_void_p(sc.cuda_stream)))
 
         def swaps():
-            _lib.check(_lib.lib.tf_kv_gather_d2h(pool.handle, segs, 256, 0, 32, eng, C.c_void_p(sd.cuda_stream)))
-            _lib.check(_lib.lib.tf_kv_scatter_h2d(pool.handle, segs, 256, 0, 32, eng, C.c_void_p(sh.cuda_stream)))
+            _lib.check(_lib.lib.tf_kv_gather_d2h(pool.handle, segs, nbk, 0, 32, eng, C.c_void_p(sd.cuda_stream)))
+            _lib.check(_lib.lib.tf_kv_scatter_h2d(pool.handle, segs, nbk, 0, 32, eng, C.c_void_p(sh.cuda_stream)))
 
         def run(fns, reps=5):
             for f in fns:
@@ -190,7 +198,7 @@ def overlap(pool, args):
         res["sm" if eng == 0 else "ce"] = {"t_decode_ms": t_dec * 1e3, "t_swap_ms": t_swp * 1e3,
                                            "t_both_ms": t_both * 1e3, "hidden_frac": hidden,
                                            "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = 32 layers of "
-                                                   "paged attention B=64 ctx=2600; swap = 512 MiB out + 512 MiB in"}
+                                                   "paged attention B=64 ctx=2600; swap = NB x 2 MiB out + NB x 2 MiB in, concurrent"}
         print(json.dumps(res), flush=True)
     return res
 
@@ -201,6 +209,7 @@ def main():
     ap.add_argument("--host-blocks", type=int, default=8192)
     ap.add_argument("--engines", default="0,1")
     ap.add_argument("--overlap", action="store_true")
+    ap.add_argument("--overlap-blocks", type=int, default=96)
     ap.add_argument("--out", default="gpurun_out/swap_sweep.json")
     args = ap.parse_args()
     args.engines = [int(x) for x in args.engines.split(",")]

@@ -126,6 +126,7 @@ class GpuDataPlane:
             self.s_evict = torch.cuda.Stream(device=dev)
             self.s_load = torch.cuda.Stream(device=dev)
         self._pending_table = []  # (row, lb, block) not yet applied on device
+        self._appending = {}  # rid -> position reserved by the in-flight decode step
         self._d2h_busy = None  # (rid, lo, hi, kind, event)
         self._last_d2h_event = {}  # rid -> event of its last d2h (loads of that range wait on it)
         self._quarantine: deque = deque()  # (event, [blocks]) realtime frees awaiting their fence
@@ -258,6 +259,8 @@ class GpuDataPlane:
         f = self.flags[rid]
         m = (f & RESERVED) != 0
         f[m] = (f[m] & CLR_RESERVED) | LIVE
+        if self.model is not None and self.kv_source == "model":
+            self.model.fill_commit(rid)
 
     def decode_start(self, batch, eng):
         spans = []
@@ -267,6 +270,7 @@ class GpuDataPlane:
             if eng.debug_checks and not (f[:p] & LIVE).all():
                 raise _lib.InvariantError(f"decode of {rid} reads non-resident KV")
             f[p] |= RESERVED
+            self._appending[rid] = p
             if p % self.B == 0 or self.gtab[rid][p // self.B] < 0:
                 self._reconcile(rid, [p // self.B])
             spans.append((rid, p, p + 1))
@@ -286,12 +290,12 @@ class GpuDataPlane:
             self.model.decode_commit(made)
         for rid in batch:
             f = self.flags[rid]
-            idx = np.nonzero(f & RESERVED)[0]
+            p = self._appending.pop(rid)  # the one position this step reserved
             if rid in made:
-                f[idx] = (f[idx] & CLR_RESERVED) | LIVE
+                f[p] = (f[p] & CLR_RESERVED) | LIVE
             else:
-                f[idx] &= CLR_RESERVED
-                self._reconcile(rid, {int(i) // self.B for i in idx})
+                f[p] &= CLR_RESERVED
+                self._reconcile(rid, (p // self.B,))
 
     def d2h_start(self, ch, eng):
         rid = ch.owner

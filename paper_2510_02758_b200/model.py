@@ -21,6 +21,7 @@ import math
 
 import torch
 import torch.nn.functional as F
+from torch.nn.attention import SDPBackend, sdpa_kernel
 
 from . import _lib
 from ._lib import check, lib
@@ -56,6 +57,7 @@ class PagedDecoder:
         self.pending = {}  # rid -> next token to emit
         self.history = {}  # rid -> generated tokens (for recompute)
         self.prompts = {}
+        self._unresolved = {}  # rid -> (pinned buffer, column) of an in-flight prefill's t0/t1
         self.scale = 1.0 / math.sqrt(hd)
         self._ws = torch.empty(1, dtype=torch.uint8, device=self.device)
         self.steps = 0
@@ -95,47 +97,76 @@ class PagedDecoder:
 
     # ------------------------------------------------------------ forward passes
     @torch.no_grad()
-    def _prefill_seq(self, dp, rid, tokens, pos0, stream):
-        """Causal forward of ``tokens`` at positions pos0.. (fresh sequence), writing KV."""
+    def _prefill_batch(self, dp, seqs, st):
+        """One causal forward over several fresh sequences (tokens concatenated
+        for the GEMMs, attention per sequence with the flash backend), writing
+        their KV into the paged pool.  seqs: [(rid, tokens[int64 cpu], pos0)].
+        Returns the argmax token after each sequence's last position (device)."""
         s = self.s
-        n = tokens.numel()
-        pos = torch.arange(pos0, pos0 + n, device=self.device)
-        rows = torch.full((n,), rid, dtype=torch.int32, device=self.device)
-        pos32 = pos.to(torch.int32)
-        x = self.embed[tokens.to(self.device)]
+        lens = [t.numel() for _, t, _ in seqs]
+        toks = torch.cat([t for _, t, _ in seqs]).pin_memory().to(self.device, non_blocking=True)
+        meta = torch.tensor([[rid, p0 + i] for rid, t, p0 in seqs for i in range(t.numel())],
+                            dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        rows, pos32 = meta[:, 0].contiguous(), meta[:, 1].contiguous()
+        pos = pos32.long()
+        n = toks.numel()
+        G = s.n_q_heads // s.n_kv_heads
+        x = self.embed[toks]
         for li, L in enumerate(self.layers):
             h = self._rms(x, L["ln1"])
             qkv = (h @ L["wqkv"]).view(n, s.n_q_heads + 2 * s.n_kv_heads, s.head_dim)
             q = self._rope(qkv[:, : s.n_q_heads], pos)
             k = self._rope(qkv[:, s.n_q_heads: s.n_q_heads + s.n_kv_heads], pos).contiguous()
             v = qkv[:, s.n_q_heads + s.n_kv_heads:].contiguous()
-            self._append(dp, rows, pos32, li, k.view(n, -1), v.view(n, -1), stream)
-            a = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k.transpose(0, 1)[None],
-                                               v.transpose(0, 1)[None], is_causal=True, enable_gqa=True)
-            x = x + a[0].transpose(0, 1).reshape(n, -1) @ L["wo"]
+            self._append(dp, rows, pos32, li, k.view(n, -1), v.view(n, -1), st)
+            outs, o = [], 0
+            with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION]):
+                for ln in lens:
+                    qi = q[o:o + ln].transpose(0, 1)[None]
+                    ki = k[o:o + ln].repeat_interleave(G, dim=1).transpose(0, 1)[None]
+                    vi = v[o:o + ln].repeat_interleave(G, dim=1).transpose(0, 1)[None]
+                    outs.append(F.scaled_dot_product_attention(qi, ki, vi, is_causal=True)[0].transpose(0, 1))
+                    o += ln
+            a = torch.cat(outs).reshape(n, -1)
+            x = torch.addmm(x, a, L["wo"])
             x = self._mlp(x, L)
-        return (self._rms(x[-1:], self.ln_f) @ self.lm_head).argmax(-1)
+        last = torch.tensor(list(_cumsum(lens)), device=self.device) - 1
+        return (self._rms(x[last], self.ln_f) @ self.lm_head).argmax(-1)
 
     @torch.no_grad()
     def prefill(self, dp, job, spans, eng):
+        """A prefill job: prompts (+ t0 decode) or recomputes; no host syncs."""
         st = dp.s_compute
         with torch.cuda.stream(st):
+            seqs = []
             for rid, lo, hi in spans:
                 spec = eng.state[rid].spec
-                if job.kind == "recompute":
-                    toks = torch.cat([self.prompt_tokens(rid, spec.prompt_len),
-                                      torch.tensor(self.history.get(rid, []), dtype=torch.long)])[: hi - lo]
-                    self._prefill_seq(dp, rid, toks, 0, st)
-                    continue
-                if job.kind == "chunk" and not job.emits_first_token:
-                    toks = self.prompt_tokens(rid, spec.prompt_len)[lo:hi]
-                    self._prefill_seq(dp, rid, toks, lo, st)  # chunked prefill (baseline policy)
-                    continue
                 prompt = self.prompt_tokens(rid, spec.prompt_len)
-                t0 = self._prefill_seq(dp, rid, prompt[lo:], lo, st) if hi - 1 > lo else prompt[-1:].to(self.device)
-                t1 = self._decode_rows(dp, [rid], t0.view(1), [hi - 1], st)
-                self.history[rid] = [int(t0.item())]
-                self.pending[rid] = int(t1[0].item())
+                if job.kind == "recompute":
+                    hist = torch.tensor(self.history.get(rid, []), dtype=torch.long)
+                    seqs.append((rid, torch.cat([prompt, hist])[: hi - lo], 0))
+                elif job.kind == "chunk":
+                    raise NotImplementedError("chunked prefill (baseline 'chunked' policy) needs prefix attention; "
+                                              "use the synthetic KV source for that baseline")
+                else:
+                    seqs.append((rid, prompt[lo: hi - 1], lo))
+            t0 = self._prefill_batch(dp, seqs, st)
+            if job.kind == "recompute":
+                return
+            rids = [r for r, _, _ in seqs]
+            t1 = self._decode_rows(dp, rids, t0, [hi - 1 for _, _, hi in spans], st)
+            buf = torch.empty((2, len(rids)), dtype=torch.long, pin_memory=True)
+            buf[0].copy_(t0, non_blocking=True)
+            buf[1].copy_(t1, non_blocking=True)
+            for i, rid in enumerate(rids):
+                self._unresolved[rid] = (buf, i)
+
+    def fill_commit(self, rid):
+        """Prefill job finished (its end event fired): t0 emitted, t1 pending."""
+        if rid in self._unresolved:
+            buf, i = self._unresolved.pop(rid)
+            self.history[rid] = [int(buf[0, i])]
+            self.pending[rid] = int(buf[1, i])
 
     @torch.no_grad()
     def decode(self, dp, batch, eng):
@@ -144,14 +175,16 @@ class PagedDecoder:
         with torch.cuda.stream(st):
             toks = torch.tensor([self.pending[r] for r in batch], dtype=torch.long).pin_memory()
             nxt = self._decode_rows(dp, list(batch), toks.to(self.device, non_blocking=True), pos, st)
-            self._last = (list(batch), nxt)
+            host = torch.empty(len(batch), dtype=torch.long, pin_memory=True)
+            host.copy_(nxt, non_blocking=True)  # sampled ids -> client (D2H of the step's result)
+            self._last = (list(batch), host)
         self.steps += 1
 
     def decode_commit(self, made):
         """Host side of a finished decode step: emit pending tokens of members that produced."""
-        batch, nxt = self._last
-        host = nxt.cpu().tolist()
-        for rid, t in zip(batch, host):
+        batch, host = self._last
+        vals = host.tolist()
+        for rid, t in zip(batch, vals):
             if rid in made:
                 self.history.setdefault(rid, []).append(self.pending[rid])
                 self.pending[rid] = t
@@ -199,3 +232,10 @@ class PagedDecoder:
             x = torch.addmm(x, attn.view(B, -1), L["wo"])
             x = self._mlp(x, L)
         return (self._rms(x, self.ln_f) @ self.lm_head).argmax(-1)
+
+
+def _cumsum(xs):
+    acc = 0
+    for x in xs:
+        acc += x
+        yield acc
