@@ -122,16 +122,16 @@ def _sum_over_ranks(x: float, world: int, device) -> float:
     return float(t.item())
 
 
-def _trace_for_rank(rank, world):
-    from paper_2510_02758_b200.workload import RequestSpec, Trace, load_trace
+def _trace_for_rank(rank, world, arrivals="burst"):
+    from paper_2510_02758_b200 import replicas
+    from paper_2510_02758_b200.workload import load_trace
 
-    tr = load_trace(str(ROOT / "tests" / "golden" / "traces" / "c2_poisson256_s1.csv"))
+    name = "c2_burst256_s1" if arrivals == "burst" else "c2_poisson256_s1"
+    tr = load_trace(str(ROOT / "tests" / "golden" / "traces" / f"{name}.csv"))
     if world == 1:
         return tr
-    # C3: the trace scaled per GPU - every replica serves a full 256-request
-    # population (ids re-densified), request i of the scaled job -> GPU i mod N
-    return Trace(tuple(RequestSpec(r.id, r.arrival_time, r.prompt_len, r.output_len, r.consume_rate)
-                       for r in tr.requests))
+    # C3: the burst scaled per GPU (256 requests per replica), request i -> GPU i mod N
+    return replicas.partition(replicas.scale_trace(tr, world), rank, world)[0]
 
 
 def run_ours(args):
@@ -141,6 +141,7 @@ def run_ours(args):
     from paper_2510_02758_b200.costs import CostModel
     from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
     from paper_2510_02758_b200.engine import SimConfig
+    from paper_2510_02758_b200.metrics import ttft_latency_stats
     from paper_2510_02758_b200.model import PagedDecoder
     from paper_2510_02758_b200.realtime import RealtimeEngine
     from paper_2510_02758_b200.scheduler import BufferAwarePolicy, SchedulerConfig
@@ -154,51 +155,45 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     c2 = configs.C2
     shape = c2.model
-    tr = _trace_for_rank(rank, world)
-    n_blocks = math.ceil(c2.gpu_mem_tokens / 16) + 4 * len(tr.requests) + c2.max_batch
+    tr = _trace_for_rank(rank, world, args.arrivals)
+    n_blocks = math.ceil(c2.gpu_mem_tokens / 16) + 4 * len(tr.requests) + c2.max_batch + 1
     pool = KvPool(n_blocks, args.host_blocks, shape.n_layers, shape.n_kv_heads, shape.head_dim, device=dev)
     model = PagedDecoder(shape, device=dev, seed=rank)
     dp = GpuDataPlane(tr.requests, pool, mode="realtime", kv_source="model", model=model,
                       n_q_heads=shape.n_q_heads, engine=args.swap_engine)
+    if args.graphs:
+        dp.enable_scratch()
+        model.enable_graphs(dp)
     policy = BufferAwarePolicy(c2.sched_cfg(SchedulerConfig))
     sim = c2.sim_cfg(SimConfig, debug_checks=False)
     cm = c2.cost_model(CostModel)
 
     t_start = time.perf_counter()
-    state = {"phase": "ff", "t_warm": None, "timed": [], "wall0": None, "wall1": None, "attn": []}
+    state = {"phase": "warm", "timed": [], "wall0": None, "wall1": None}
 
     def on_step(rec, eng):
-        contended = eng.total_preemptions > 0
-        if args.verbose and len(eng.steps) % 200 == 0:
-            print(f"[bench] step {len(eng.steps)} t={eng.now:.2f}s batch={rec['batch']} dur={rec['dur'] * 1e3:.2f}ms "
+        n = len(eng.steps)
+        if args.verbose and n % 100 == 0:
+            print(f"[bench] step {n} t={eng.now:.2f}s batch={rec['batch']} dur={rec['dur'] * 1e3:.2f}ms "
                   f"pre={eng.total_preemptions} rc={eng.total_recomputes} running={len(eng.running)} "
                   f"waiting={len(eng.waiting)} d2h={dp.stats['d2h_tokens']} h2d={dp.stats['h2d_tokens']} "
                   f"wall={time.perf_counter() - t_start:.1f}s", file=sys.stderr, flush=True)
-        if state["phase"] == "ff":
-            if contended or len(eng.steps) >= args.ff_max:
-                state["phase"] = "warm"
-                state["warm_left"] = args.warmup
-                state["ff_steps"] = len(eng.steps)
-            return
         if state["phase"] == "warm":
-            state["warm_left"] -= 1
-            if state["warm_left"] <= 0:
+            if n >= args.warmup:
                 state["phase"] = "timed"
                 state["wall0"] = time.perf_counter()
-                state["d2h0"], state["h2d0"] = dp.stats["d2h_tokens"], dp.stats["h2d_tokens"]
                 state["ev0"] = len(dp._events)
-                model.attn_timing = []
+                state["pre0"], state["rc0"] = eng.total_preemptions, eng.total_recomputes
             return
         if state["phase"] == "timed":
             state["timed"].append(dict(rec))
             if len(state["timed"]) >= args.steps:
                 state["wall1"] = time.perf_counter()
-                state["d2h1"], state["h2d1"] = dp.stats["d2h_tokens"], dp.stats["h2d_tokens"]
                 state["ev1"] = len(dp._events)
-                state["attn"] = list(getattr(model, "attn_timing", []))
-                model.attn_timing = None
+                state["pre1"], state["rc1"] = eng.total_preemptions, eng.total_recomputes
                 state["phase"] = "done"
-                eng._stop = True
+                if not args.full_run:
+                    eng._stop = True
 
     eng = RealtimeEngine(tr, policy, cm, sim, dp, skip_idle=True, on_step=on_step)
     if world > 1:
@@ -228,29 +223,33 @@ def run_ours(args):
     h2d_tok = sum(n for k, n, _ in xfers if k == "h2d")
     d2h_ms = sum(ms for k, _, ms in xfers if k == "d2h")
     h2d_ms = sum(ms for k, _, ms in xfers if k == "h2d")
-    swap = {
-        "d2h_tokens": d2h_tok, "h2d_tokens": h2d_tok,
-        "d2h_gbs": (d2h_tok * bpt / (d2h_ms / 1e3) / 1e9) if d2h_ms else None,
-        "h2d_gbs": (h2d_tok * bpt / (h2d_ms / 1e3) / 1e9) if h2d_ms else None,
-        "pcie_gen5_gbs": PCIE_GEN5_GBS,
-    }
+    swap = {"d2h_tokens": d2h_tok, "h2d_tokens": h2d_tok, "chunks": len(xfers),
+            "engine": "copy-engine batch" if args.swap_engine == 1 else "SM kernel",
+            "d2h_gbs": (d2h_tok * bpt / (d2h_ms / 1e3) / 1e9) if d2h_ms else None,
+            "h2d_gbs": (h2d_tok * bpt / (h2d_ms / 1e3) / 1e9) if h2d_ms else None,
+            "pcie_gen5_gbs": PCIE_GEN5_GBS,
+            "preemptions": state["pre1"] - state["pre0"], "recomputes": state["rc1"] - state["rc0"]}
     for k in ("d2h", "h2d"):
         if swap[f"{k}_gbs"]:
             swap[f"{k}_frac_pcie"] = swap[f"{k}_gbs"] / PCIE_GEN5_GBS
-    # roofline of the dominant hand-written kernel: paged decode attention
+    # roofline of the dominant hand-written kernel (paged decode attention),
+    # timed with CUDA events on the live pool: the largest timed batch's
+    # members that are still resident, all 32 layers
     hbm, peak_kind = _peaks()
-    attn = state["attn"]
     roof = None
-    if attn:
-        per = [(b, e0.elapsed_time(e1)) for b, e0, e1 in attn]
+    big = max(timed, key=lambda r: r["batch"])
+    live = [r for r in big["rids"] if eng.state[r].status == "running"]
+    if live:
+        per = model.measure_attention(dp, live, [eng.state[r].kv.total_kv - 1 for r in live])
         avg_ms = sum(ms for _, ms in per) / len(per)
         avg_bytes = sum(b for b, _ in per) / len(per)
         ach = avg_bytes / (avg_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "paged_attn_kernel<128,4>", "achieved": round(ach, 1),
-                "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4),
-                "traffic": None, "launches": len(per), "avg_ms": round(avg_ms, 4),
-                "algorithmic_bytes_per_launch": round(avg_bytes)}
-    h2d_step = sum(s.get("h2d_bytes", 0) for s in timed)
+        roof = {"bound": "hbm", "kernel": "paged_attn_tma_kernel<128,4> (+combine)", "achieved": round(ach, 1),
+                "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
+                "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live),
+                "algorithmic_bytes_per_launch": round(avg_bytes),
+                "note": "bytes = sum(ctx) x 4 KiB (K+V, 8 kv heads x 128 x bf16) + q/out + table entries per layer"}
+    ttft = [r for r in res.records if r.gen_times]
     out = {
         "metric": METRIC,
         "value": eff / dev_s if dev_s > 0 else None,
@@ -264,28 +263,35 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init Llama3-8B weights, seeded prompt token ids, frozen C2 trace)",
-        "config": {"workload": "C2: Llama3-8B bf16 random-init, 1xB200 per replica, 256-request Poisson burst "
-                               "(lambda=10/s, first 256 of a 30 s trace, seed 1), KV pool 163,840 tokens (20 GiB) "
-                               "with swap to pinned host, block 16",
-                   "model": "llama3-8b", "global_batch": timed and max(s["batch"] for s in timed),
-                   "seq_len": None, "parallelism": f"replicas x{world}",
+        "config": {"workload": f"C2: Llama3-8B bf16 random-init, 1xB200 per replica, 256-request {args.arrivals} "
+                               "(bodies of the first 256 arrivals of the lambda=10/s 30 s trace, seed 1), KV pool "
+                               "163,840 tokens (20 GiB) + pinned host tier, block 16, max_batch 128",
+                   "model": "llama3-8b", "global_batch": max(s["batch"] for s in timed),
+                   "mean_batch": round(statistics.mean(s["batch"] for s in timed), 1),
+                   "seq_len": None, "parallelism": f"replicas x{world}", "arrivals": args.arrivals,
                    "l2": "working set (16 GB weights + KV) >> 126 MB L2; no flush needed",
-                   "timed_region": "K decode iterations after contention + W warm-up"},
+                   "timed_region": f"decode iterations [{args.warmup}, {args.warmup + args.steps}) from t=0 "
+                                   "of the real-time loop (measured clock, idle gaps skipped)",
+                   "cuda_graphs": bool(args.graphs)},
         "raw_tok_s": toks / dev_s if dev_s > 0 else None,
         "e2e": {"value": eff / wall if wall > 0 else None, "unit": "effective tok/s",
-                "h2d_bytes_per_step": int((h2d_tok * bpt + len(timed) * 0) / max(1, len(timed))),
-                "d2h_bytes_per_step": int(d2h_tok * bpt / max(1, len(timed)))},
+                "h2d_bytes_per_step": int((h2d_tok * bpt + sum(s["batch"] for s in timed) * 24) / len(timed)),
+                "d2h_bytes_per_step": int((d2h_tok * bpt + sum(s["batch"] for s in timed) * 8) / len(timed))},
         "swap": swap,
         "roofline": roof,
         "clocks": sampler.summary(),
         "gpu_launches": None,
-        "fast_forward_steps": state.get("ff_steps"),
-        "preemptions_so_far": res.total_preemptions,
+        "first_tokens_in_window": len(ttft),
     }
-    launches = dp.stats
-    out["gpu_launches"] = int(len(timed) * (shape.n_layers * 2) + len(xfers))
-    out["e2e"]["h2d_bytes_per_step"] += int(sum(s["batch"] for s in timed) * 12 / max(1, len(timed)))
-    out["e2e"]["d2h_bytes_per_step"] += int(sum(s["batch"] for s in timed) * 8 / max(1, len(timed)))
+    out["gpu_launches"] = int(len(timed) * shape.n_layers * (3 if args.graphs else 2) + len(xfers))
+    if args.full_run:
+        from paper_2510_02758_b200.metrics import EffectiveThroughputConfig, effective_throughput
+
+        out["full_run"] = {"effective_tok_s": effective_throughput(res.records, res.total_time,
+                                                                   EffectiveThroughputConfig()),
+                           "ttft_latency": ttft_latency_stats(res.records), "total_time_s": res.total_time,
+                           "wall_s": eng.wall_s, "preemptions": res.total_preemptions,
+                           "recomputes": res.total_recomputes}
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, timed, quick=True)
     if rank == 0:
@@ -325,12 +331,14 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--host-blocks", type=int, default=int(os.environ.get("TF_HOST_BLOCKS", 26000)))
     ap.add_argument("--swap-engine", type=int, default=1)
-    ap.add_argument("--ff-max", type=int, default=6000)
+    ap.add_argument("--arrivals", default="burst", choices=["burst", "poisson"])
+    ap.add_argument("--graphs", type=int, default=1)
+    ap.add_argument("--full-run", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-batch", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")

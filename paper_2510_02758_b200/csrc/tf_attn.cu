@@ -284,10 +284,287 @@ __global__ void attn_combine_kernel(const AttnArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------
+// v2: TMA bulk-copy pipeline.  Warp 0 is the producer: one elected lane
+// streams each block's contiguous K tile and V tile (16 x head_dim bf16 each)
+// into an S-stage shared-memory ring with cp.async.bulk (the TMA engine does
+// the address generation; no register staging), signalling mbarriers with the
+// transaction bytes.  Warps 1..4 consume stages round-robin with the same
+// math as v1, reading conflict-free 16-B rows from shared memory, and release
+// each stage through an "empty" mbarrier.  Bytes in flight per CTA = S x 8 KiB.
+constexpr int kStages = 8;
+constexpr int kConsumers = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__((kConsumers + 1) * 32) paged_attn_tma_kernel(const AttnArgs a) {
+  constexpr int LPR = D / 8;
+  constexpr int TPP = 32 / LPR;
+  constexpr int ITER = kBlk / TPP;
+  constexpr int GP = Pow2Ceil<G>::v > LPR / ITER ? Pow2Ceil<G>::v : LPR / ITER;
+  constexpr int NV = ITER * GP;
+  constexpr int NR = NV / LPR;
+  constexpr uint32_t kTile = kBlk * D * 2;  // bytes of one K or V tile
+  static_assert(NV % LPR == 0 && NR >= 1, "unsupported (D, G)");
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint16_t* kv_sh = reinterpret_cast<uint16_t*>(smem_raw);  // [kStages][2][kBlk*D]
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ float p_sh[kConsumers][kBlk][GP];
+  __shared__ float m_sh[kConsumers][G], l_sh[kConsumers][G];
+  __shared__ float acc_sh[kConsumers][G][D];
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int bh = blockIdx.y;
+  const int b = bh / a.kv_heads, kvh = bh % a.kv_heads;
+  const int split = blockIdx.x;
+  const int ctx = a.ctx[b];
+  const int nblk = (ctx + kBlk - 1) / kBlk;
+  const int blk_lo = split * a.blocks_per_split;
+  const int blk_hi = min(nblk, blk_lo + a.blocks_per_split);
+  const int nloc = max(0, blk_hi - blk_lo);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t tile = (int64_t)kBlk * D;
+  const int64_t koff = (((int64_t)a.layer * 2 + 0) * a.kv_heads + kvh) * tile;
+  const int64_t voff = (((int64_t)a.layer * 2 + 1) * a.kv_heads + kvh) * tile;
+  const int32_t* trow = a.table + (int64_t)a.rows[b] * a.stride;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (int i = 0; i < nloc; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) mbar_wait(&empty_bar[s], ((i / kStages) - 1) & 1);
+        const int64_t base = (int64_t)__ldg(trow + blk_lo + i) * a.block_elems;
+        uint16_t* dst = kv_sh + (int64_t)s * 2 * tile;
+        mbar_expect_tx(&full_bar[s], 2 * kTile);
+        tma_bulk_g2s(dst, a.pool + base + koff, kTile, &full_bar[s]);
+        tma_bulk_g2s(dst + tile, a.pool + base + voff, kTile, &full_bar[s]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    const int c = warp - 1;
+    const int col = (lane % LPR) * 8;
+    const int rsub = lane / LPR;
+    float qf[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int h = kvh * G + g;
+      uint4 u = *reinterpret_cast<const uint4*>(a.q + ((int64_t)b * a.hq + h) * D + col);
+      bf16x8_to_f32(u, qf[g]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) qf[g][j] *= a.scale_log2;
+    }
+    float m[G], l[G], acc[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      m[g] = -FLT_MAX;
+      l[g] = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[g][j] = 0.f;
+    }
+    for (int i = c; i < nloc; i += kConsumers) {
+      const int s = i % kStages;
+      const int blk = blk_lo + i;
+      mbar_wait(&full_bar[s], (i / kStages) & 1);
+      const uint16_t* kt = kv_sh + (int64_t)s * 2 * tile;
+      const uint16_t* vt = kt + tile;
+      float val[NV];
+#pragma unroll
+      for (int it = 0; it < ITER; ++it) {
+        const int t = it * TPP + rsub;
+        float kf[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(kt + t * D + col), kf);
+#pragma unroll
+        for (int g = 0; g < GP; ++g) {
+          float sacc = 0.f;
+          if (g < G) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sacc = fmaf(qf[g][j], kf[j], sacc);
+          }
+          val[it * GP + g] = sacc;
+        }
+      }
+      int cnt = NV;
+#pragma unroll
+      for (int off = LPR / 2; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+        const int half = cnt / 2;
+#pragma unroll
+        for (int k = 0; k < NV / 2; ++k) {
+          if (k < half) {
+            float send = upper ? val[k] : val[k + half];
+            float keep = upper ? val[k + half] : val[k];
+            val[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+          }
+        }
+        cnt = half;
+      }
+      const int x = lane % LPR;
+      float bm[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) bm[g] = -FLT_MAX;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int fi = x * NR + r;
+        const int g = fi % GP, t = (fi / GP) * TPP + rsub;
+        if (!((g < G) && (blk * kBlk + t < ctx))) val[r] = -FLT_MAX;
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+          if (g == gg) bm[gg] = fmaxf(bm[gg], val[r]);
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) bm[g] = fmaxf(bm[g], __shfl_xor_sync(0xffffffffu, bm[g], off));
+        const float mn = fmaxf(m[g], bm[g]);
+        const float alpha = exp2f(m[g] - mn);
+        m[g] = mn;
+        l[g] *= alpha;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[g][j] *= alpha;
+      }
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int fi = x * NR + r;
+        const int g = fi % GP, t = (fi / GP) * TPP + rsub;
+        float p = 0.f;
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+          if (g == gg && val[r] > -FLT_MAX) p = exp2f(val[r] - m[gg]);
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+          if (g == gg) l[gg] += p;
+        p_sh[c][t][g] = p;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < ITER; ++it) {
+        const int t = it * TPP + rsub;
+        if (blk * kBlk + t >= ctx) continue;
+        float vf[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(vt + t * D + col), vf);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float p = p_sh[c][t][g];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[g][j] = fmaf(p, vf[j], acc[g][j]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) l[g] += __shfl_xor_sync(0xffffffffu, l[g], off);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+#pragma unroll
+        for (int off = 16; off >= LPR; off >>= 1) acc[g][j] += __shfl_xor_sync(0xffffffffu, acc[g][j], off);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        m_sh[c][g] = m[g];
+        l_sh[c][g] = l[g];
+      }
+    }
+    if (rsub == 0) {
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc_sh[c][g][col + j] = acc[g][j];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
+    const int g = e / D, d = e % D;
+    float mm = -FLT_MAX;
+#pragma unroll
+    for (int w = 0; w < kConsumers; ++w) mm = fmaxf(mm, m_sh[w][g]);
+    float ll = 0.f, aa = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumers; ++w) {
+      const float f = (m_sh[w][g] == -FLT_MAX) ? 0.f : exp2f(m_sh[w][g] - mm);
+      ll += l_sh[w][g] * f;
+      aa += acc_sh[w][g][d] * f;
+    }
+    const int h = kvh * G + g;
+    const int64_t row = (int64_t)b * a.hq + h;
+    if (a.splits == 1) {
+      a.out[row * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(ll > 0.f ? aa / ll : 0.f));
+    } else {
+      a.ws_acc[(row * a.splits + split) * D + d] = aa;
+      if (d == 0) {
+        a.ws_ml[(row * a.splits + split) * 2 + 0] = mm;
+        a.ws_ml[(row * a.splits + split) * 2 + 1] = ll;
+      }
+    }
+  }
+}
+
+static int attn_impl() {
+  static int impl = -1;
+  if (impl < 0) {
+    const char* e = getenv("TF_ATTN_IMPL");
+    impl = (e && e[0] == '1') ? 1 : 2;
+  }
+  return impl;
+}
+
 static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps) {
   const int nblk = std::max(1, (max_ctx + kBlk - 1) / kBlk);
   const int base = std::max(1, B * kv_heads);
-  const int target = 148 * 6;  // resident CTAs per wave (4 warps each)
+  // >= ~4 waves of resident CTAs (3 per SM) so the tail wave is cheap,
+  // >= 8 blocks per split so the pipeline prologue is amortised
+  const int target = attn_impl() == 2 ? 148 * 3 * 4 : 148 * 6;
   int s = std::max(1, std::min((target + base - 1) / base, (nblk + 7) / 8));
   int per = (nblk + s - 1) / s;
   s = (nblk + per - 1) / per;
@@ -298,7 +575,17 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
 template <int D, int G>
 static int launch(const AttnArgs& a, int B, cudaStream_t st) {
   dim3 grid(a.splits, B * a.kv_heads);
-  paged_attn_kernel<D, G><<<grid, kAttnWarps * 32, 0, st>>>(a);
+  if (attn_impl() == 2) {
+    const int smem = kStages * 2 * kBlk * D * 2;
+    static bool attr = false;
+    if (!attr) {
+      TF_CUDA(cudaFuncSetAttribute(paged_attn_tma_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    paged_attn_tma_kernel<D, G><<<grid, (kConsumers + 1) * 32, smem, st>>>(a);
+  } else {
+    paged_attn_kernel<D, G><<<grid, kAttnWarps * 32, 0, st>>>(a);
+  }
   TF_LAUNCH_CHECK();
   if (a.splits > 1) {
     attn_combine_kernel<D><<<B * a.hq, std::min(D, 128), 0, st>>>(a);

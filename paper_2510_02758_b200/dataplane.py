@@ -118,7 +118,10 @@ class GpuDataPlane:
         self.gtab = {r.id: np.full(self.nlb, -1, np.int32) for r in reqs}
         self.htab = {r.id: np.full(self.nlb, -1, np.int32) for r in reqs}
         self.host_hi = {r.id: 0 for r in reqs}
-        self.table = torch.full((n_rows, self.nlb), -1, dtype=torch.int32, device=dev)
+        # one extra row: padding rows of graph-captured decode steps point there
+        self.table = torch.full((n_rows + 1, self.nlb), -1, dtype=torch.int32, device=dev)
+        self.scratch_row = n_rows
+        self.scratch_block = None
         if mode == "replay":
             self.s_compute = self.s_evict = self.s_load = torch.cuda.Stream(device=dev)
         else:
@@ -138,6 +141,14 @@ class GpuDataPlane:
         ws = max(1, int(lib.tf_paged_decode_attn_workspace(pool.handle, max(1, len(reqs)), self.max_len, 64)))
         self._attn_ws = torch.empty(ws, dtype=torch.uint8, device=dev)
         self.attn_out = None
+
+    def enable_scratch(self):
+        """Reserve one block for the padding rows of captured decode graphs."""
+        if self.scratch_block is None:
+            self.scratch_block = self._alloc_blocks(1)[0]
+            self.table[self.scratch_row].fill_(self.scratch_block)
+            torch.cuda.synchronize()
+        return self.scratch_block
 
     # ------------------------------------------------------------ block table
     def _reconcile(self, rid, blocks):

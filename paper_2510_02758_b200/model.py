@@ -62,6 +62,7 @@ class PagedDecoder:
         self._ws = torch.empty(1, dtype=torch.uint8, device=self.device)
         self.steps = 0
         self.attn_timing = None  # list -> (algorithmic bytes, start event, end event) per attention launch
+        self._graphs = {}
 
     # ------------------------------------------------------------ pieces
     def prompt_tokens(self, rid: int, n: int) -> torch.Tensor:
@@ -173,8 +174,12 @@ class PagedDecoder:
         st = dp.s_compute
         pos = [eng.state[r].kv.total_kv for r in batch]
         with torch.cuda.stream(st):
-            toks = torch.tensor([self.pending[r] for r in batch], dtype=torch.long).pin_memory()
-            nxt = self._decode_rows(dp, list(batch), toks.to(self.device, non_blocking=True), pos, st)
+            if self._graphs and len(batch) <= max(self._graphs) and self.attn_timing is None:
+                nxt = self._decode_graph(dp, list(batch), pos, st)
+            else:
+                toks = torch.tensor([self.pending[r] for r in batch], dtype=torch.long).pin_memory()
+                nxt = self._decode_rows(dp, list(batch), toks.to(self.device, non_blocking=True), pos, st)
+            dp.stats["attn_launches"] += self.s.n_layers
             host = torch.empty(len(batch), dtype=torch.long, pin_memory=True)
             host.copy_(nxt, non_blocking=True)  # sampled ids -> client (D2H of the step's result)
             self._last = (list(batch), host)
@@ -189,20 +194,110 @@ class PagedDecoder:
                 self.history.setdefault(rid, []).append(self.pending[rid])
                 self.pending[rid] = t
 
+    @torch.no_grad()
+    def measure_attention(self, dp, rids, positions, reps=3):
+        """Time the paged-attention kernel on a live batch (all layers, CUDA
+        events on the launching stream) -> [(algorithmic bytes, ms)] per launch."""
+        s = self.s
+        st = dp.s_compute
+        B = len(rids)
+        with torch.cuda.stream(st):
+            rows = torch.tensor(rids, dtype=torch.int32, device=self.device)
+            ctx = torch.tensor([p + 1 for p in positions], dtype=torch.int32, device=self.device)
+            q = torch.randn((B, s.n_q_heads, s.head_dim), device=self.device).to(torch.bfloat16)
+            out = torch.empty_like(q)
+            max_ctx = max(positions) + 1
+            ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, s.n_q_heads)))
+            ws = torch.empty(ws_n, dtype=torch.uint8, device=self.device)
+            abytes = (sum(positions) + B) * 2 * s.n_kv_heads * s.head_dim * 2 + 2 * B * s.n_q_heads * s.head_dim * 2 \
+                + sum((p + 16) // 16 for p in positions) * 4
+            res = []
+            for r in range(reps + 1):
+                for li in range(s.n_layers):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                    check(lib.tf_paged_decode_attn(dp.pool.handle, C.c_void_p(q.data_ptr()),
+                                                   C.c_void_p(dp.table.data_ptr()), dp.nlb,
+                                                   C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B,
+                                                   max_ctx, li, s.n_q_heads, self.scale, C.c_void_p(out.data_ptr()),
+                                                   C.c_void_p(ws.data_ptr()), ws_n, C.c_void_p(st.cuda_stream)),
+                          "tf_paged_decode_attn")
+                    e1.record(st)
+                    if r > 0:  # first pass is warm-up
+                        res.append((abytes, e0, e1))
+        st.synchronize()
+        return [(b, e0.elapsed_time(e1)) for b, e0, e1 in res]
+
+    # ------------------------------------------------------------ CUDA graphs
+    def enable_graphs(self, dp, buckets=(8, 16, 24, 32, 48, 64, 80, 96, 112, 128)):
+        """Capture the decode forward once per batch-size bucket.
+
+        Shapes are static per bucket: padded rows point at a scratch table row
+        (one reserved block), attention is planned for the pool's maximum
+        context (rows shorter than that exit their empty split CTAs early).
+        A step then costs one H2D of [tokens, rows, positions], one graph
+        launch and one D2H of the sampled ids.
+        """
+        s = self.s
+        self._gdp = dp
+        self._gmax_ctx = dp.nlb * dp.B
+        self._graphs = {}
+        mempool = torch.cuda.graph_pool_handle()
+        st = dp.s_compute
+        for Bp in buckets:
+            io = torch.zeros((3, Bp), dtype=torch.int64, device=self.device)
+            io[1].fill_(dp.scratch_row)
+            stage = torch.zeros((3, Bp), dtype=torch.int64, pin_memory=True)
+            ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, Bp, self._gmax_ctx, s.n_q_heads)))
+            ws = torch.empty(ws_n, dtype=torch.uint8, device=self.device)
+            with torch.cuda.stream(st):
+                self._forward_graphable(dp, io, Bp, ws, st)  # warm-up (kernel attributes, cuBLAS handles)
+            st.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=mempool, stream=st):
+                out = self._forward_graphable(dp, io, Bp, ws, torch.cuda.current_stream())
+            self._graphs[Bp] = (g, io, stage, out, ws)
+        st.synchronize()
+
+    def _forward_graphable(self, dp, io, Bp, ws, st):
+        rows = io[1].to(torch.int32)
+        pos32 = io[2].to(torch.int32)
+        ctx = pos32 + 1
+        return self._layers_decode(dp, io[0], rows, pos32, ctx, Bp, self._gmax_ctx, ws, st, timing=None)
+
+    def _decode_graph(self, dp, rids, positions, st):
+        B = len(rids)
+        Bp = next(b for b in sorted(self._graphs) if b >= B)
+        g, io, stage, out, _ = self._graphs[Bp]
+        stage[0, :B] = torch.tensor([self.pending[r] for r in rids])
+        stage[0, B:] = 0
+        stage[1, :B] = torch.tensor(rids)
+        stage[1, B:] = dp.scratch_row
+        stage[2, :B] = torch.tensor(positions)
+        stage[2, B:] = 0
+        with torch.cuda.stream(st):
+            io.copy_(stage, non_blocking=True)
+            g.replay()
+        # the staging buffer is reused next step only after this step completed
+        return out[:B]
+
     def _decode_rows(self, dp, rids, tokens, positions, st):
         s = self.s
         B = len(rids)
         rows = torch.tensor(rids, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
         pos32 = torch.tensor(positions, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
         ctx = pos32 + 1
-        pos = pos32.long()
         max_ctx = max(positions) + 1
         need = int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, s.n_q_heads))
         if need > self._ws.numel():
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._layers_decode(dp, tokens, rows, pos32, ctx, B, max_ctx, self._ws, st, self.attn_timing,
+                                   positions)
+
+    def _layers_decode(self, dp, tokens, rows, pos32, ctx, B, max_ctx, ws, st, timing, positions=None):
+        s = self.s
         x = self.embed[tokens]
         attn = torch.empty((B, s.n_q_heads, s.head_dim), device=self.device, dtype=x.dtype)
-        timing = self.attn_timing
         if timing is not None:
             # algorithmic bytes of one launch: K+V of every context token, q in,
             # out, block-table entries (SURVEY.md 8d)
@@ -223,12 +318,11 @@ class PagedDecoder:
             check(lib.tf_paged_decode_attn(dp.pool.handle, C.c_void_p(q.data_ptr()), C.c_void_p(dp.table.data_ptr()),
                                            dp.nlb, C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B, max_ctx,
                                            li, s.n_q_heads, self.scale, C.c_void_p(attn.data_ptr()),
-                                           C.c_void_p(self._ws.data_ptr()), self._ws.numel(),
+                                           C.c_void_p(ws.data_ptr()), ws.numel(),
                                            C.c_void_p(st.cuda_stream)), "tf_paged_decode_attn")
             if timing is not None:
                 e1.record(st)
                 timing.append((abytes, e0, e1))
-            dp.stats["attn_launches"] += 1
             x = torch.addmm(x, attn.view(B, -1), L["wo"])
             x = self._mlp(x, L)
         return (self._rms(x, self.ln_f) @ self.lm_head).argmax(-1)

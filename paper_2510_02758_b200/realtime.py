@@ -154,7 +154,7 @@ class RealtimeEngine(Engine):
 
     def _record_step(self, batch, start, end, dur):
         self._step_pre = {r: (self.state[r].status, self.state[r].generated) for r in batch}
-        self.steps.append({"start": start, "end": end, "dur": dur, "batch": len(batch)})
+        self.steps.append({"start": start, "end": end, "dur": dur, "batch": len(batch), "rids": list(batch)})
 
     def _finish_step(self, idx):
         rec = self.steps[idx]
