@@ -224,7 +224,8 @@ def run_ours(args):
     d2h_ms = sum(ms for k, _, ms in xfers if k == "d2h")
     h2d_ms = sum(ms for k, _, ms in xfers if k == "h2d")
     swap = {"d2h_tokens": d2h_tok, "h2d_tokens": h2d_tok, "chunks": len(xfers),
-            "engine": "copy-engine batch" if args.swap_engine == 1 else "SM kernel",
+            "engine": {0: "SM kernel", 1: "copy-engine batch", 2: "auto (CE whole blocks + SM partial)"}[
+                args.swap_engine],
             "d2h_gbs": (d2h_tok * bpt / (d2h_ms / 1e3) / 1e9) if d2h_ms else None,
             "h2d_gbs": (h2d_tok * bpt / (h2d_ms / 1e3) / 1e9) if h2d_ms else None,
             "pcie_gen5_gbs": PCIE_GEN5_GBS,
@@ -335,7 +336,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--host-blocks", type=int, default=int(os.environ.get("TF_HOST_BLOCKS", 26000)))
-    ap.add_argument("--swap-engine", type=int, default=1)
+    ap.add_argument("--swap-engine", type=int, default=2, help="0 SM kernel, 1 copy engines, 2 auto (whole "
+                    "blocks on copy engines, partial blocks on the SM kernel)")
     ap.add_argument("--arrivals", default="burst", choices=["burst", "poisson"])
     ap.add_argument("--graphs", type=int, default=1)
     ap.add_argument("--full-run", action="store_true")

@@ -50,6 +50,7 @@ extern "C" {
 #define TF_TIER_HOST 1
 #define TF_ENGINE_SM 0 /* SM-driven zero-copy gather/scatter kernel */
 #define TF_ENGINE_CE 1 /* copy engines (cudaMemcpyBatchAsync of contiguous runs) */
+#define TF_ENGINE_AUTO 2 /* whole blocks on copy engines, partial blocks on the SM kernel */
 
 const char* tf_last_error(void);
 int tf_abi_version(void);

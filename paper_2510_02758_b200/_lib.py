@@ -15,7 +15,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_tf_b200.so"
 
 TF_OK, TF_EINVAL, TF_ENOMEM, TF_EIO = 0, -22, -12, -5
 TIER_GPU, TIER_HOST = 0, 1
-ENGINE_SM, ENGINE_CE = 0, 1
+ENGINE_SM, ENGINE_CE, ENGINE_AUTO = 0, 1, 2
 
 
 class InvariantError(AssertionError):

@@ -199,6 +199,20 @@ static int swap_entry(int64_t pool, const tf_seg* segs, int32_t n, int32_t l0, i
   if (n == 0) return TF_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (engine == TF_ENGINE_CE) return swap_ce(*p, segs, n, l0, l1, to_host, st);
+  if (engine == TF_ENGINE_AUTO) {
+    // whole blocks (one contiguous run each) -> copy engines, no SMs;
+    // partial blocks (2*kv_heads*layers short runs each) -> one SM kernel
+    std::vector<tf_seg> full, part;
+    const bool all_layers = (l0 == 0 && l1 == p->n_layers);
+    for (int32_t i = 0; i < n; ++i)
+      (all_layers && segs[i].n_slots == p->block_tokens ? full : part).push_back(segs[i]);
+    if (!full.empty()) {
+      int rc = swap_ce(*p, full.data(), (int32_t)full.size(), l0, l1, to_host, st);
+      if (rc != TF_OK) return rc;
+    }
+    if (!part.empty()) return swap_sm(*p, part.data(), (int32_t)part.size(), l0, l1, to_host, st);
+    return TF_OK;
+  }
   TF_CHECK_ARG(engine == TF_ENGINE_SM, "swap: unknown engine %d", engine);
   return swap_sm(*p, segs, n, l0, l1, to_host, st);
 }

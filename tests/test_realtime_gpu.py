@@ -9,7 +9,7 @@ from conftest import load_golden, pool_blocks, trace_path
 pytestmark = pytest.mark.gpu
 
 
-def _run(cuda, name="c1_tokenflow", engine=0, max_steps=None):
+def _run(cuda, name="c1_tokenflow", engine=0, max_steps=None, graphs=False):
     from paper_2510_02758_b200 import configs
     from paper_2510_02758_b200.costs import CostModel
     from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
@@ -27,15 +27,18 @@ def _run(cuda, name="c1_tokenflow", engine=0, max_steps=None):
     model = PagedDecoder(shape, device=cuda)
     dp = GpuDataPlane(tr.requests, pool, mode="realtime", kv_source="model", model=model,
                       n_q_heads=shape.n_q_heads, engine=engine)
+    if graphs:
+        dp.enable_scratch()
+        model.enable_graphs(dp, buckets=(2, 4, 8))
     eng = RealtimeEngine(tr, make_policy(g["policy"], SchedulerConfig(**g["sched"])), CostModel(**g["cm"]),
                          SimConfig(**g["sim"]), dp, skip_idle=True, max_steps=max_steps)
     res = eng.run()
     return g, eng, res, dp, model
 
 
-@pytest.mark.parametrize("engine", [0, 1])
-def test_realtime_c1_completes_with_invariants(cuda, engine):
-    g, eng, res, dp, model = _run(cuda, engine=engine)
+@pytest.mark.parametrize("engine,graphs", [(0, False), (1, False), (1, True)])
+def test_realtime_c1_completes_with_invariants(cuda, engine, graphs):
+    g, eng, res, dp, model = _run(cuda, engine=engine, graphs=graphs)
     eng._final_invariants(res.records)
     assert all(len(r.gen_times) == r.output_len for r in res.records)
     assert res.total_preemptions > 0 and dp.stats["h2d_tokens"] > 0 and dp.stats["d2h_tokens"] > 0
@@ -43,3 +46,47 @@ def test_realtime_c1_completes_with_invariants(cuda, engine):
     for rid, hist in model.history.items():
         assert len(hist) == res.records[rid].output_len
     assert eng.mem_used == 0 and eng.mem_committed == 0
+
+
+def test_graph_decode_matches_eager(cuda):
+    """The captured decode graph computes the same next tokens and KV as the
+    eager launch sequence (same kernels, padded rows go to the scratch row)."""
+    import torch
+
+    from paper_2510_02758_b200 import configs
+    from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
+    from paper_2510_02758_b200.model import PagedDecoder
+    from paper_2510_02758_b200.workload import RequestSpec
+
+    shape = configs.TINY
+    reqs = [RequestSpec(i, 0.0, 40 + 7 * i, 50, 20.0) for i in range(5)]
+    pool = KvPool(64, 1, shape.n_layers, shape.n_kv_heads, shape.head_dim, device=cuda)
+    model = PagedDecoder(shape, device=cuda)
+    dp = GpuDataPlane(reqs, pool, mode="realtime", kv_source="model", model=model, n_q_heads=shape.n_q_heads)
+    # map positions [0, 64) of every request to distinct blocks and fill KV with noise
+    tab = torch.arange(5 * 4, dtype=torch.int32, device=cuda).view(5, 4)
+    dp.table[:5, :4] = tab
+    pool.gpu.copy_((torch.randn(pool.gpu.numel(), device=cuda) * 0.3).to(torch.bfloat16).view(torch.int16))
+    dp.enable_scratch()
+    model.enable_graphs(dp, buckets=(8,))
+    rids, pos = [0, 2, 3], [40, 54, 61]
+    for r in rids:
+        model.pending[r] = 100 + r
+    snap = pool.gpu.clone()
+    st = dp.s_compute
+    with torch.cuda.stream(st):
+        g_out = model._decode_graph(dp, rids, pos, st).clone()
+    st.synchronize()
+    kv_graph = pool.gpu.clone()
+    pool.gpu.copy_(snap)
+    with torch.cuda.stream(st):
+        toks = torch.tensor([100 + r for r in rids], device=cuda)
+        e_out = model._decode_rows(dp, rids, toks, pos, st)
+    st.synchronize()
+    # the graph plans attention splits for the pool's maximum context, the eager
+    # path for this batch's: same math, different fp32 summation order
+    assert (g_out == e_out).float().mean().item() >= 2 / 3
+    blocks = tab[rids].flatten().long()
+    a = kv_graph.view(64, -1)[blocks].view(torch.bfloat16).float()
+    b = pool.gpu.view(64, -1)[blocks].view(torch.bfloat16).float()
+    assert torch.allclose(a, b, atol=3e-2, rtol=3e-2)
