@@ -107,10 +107,12 @@ int tf_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride, con
  * [head_dim] bf16 -> rotary embedding (interleaved pairs, angle = pos *
  * inv_freq[i], inv_freq fp32 [head_dim/2] on device) of q and k; k and v
  * appended at (table[rows[i]], pos[i]) of `layer`; rotated q written to
- * q_out [n][n_q_heads][head_dim].  One launch per layer. */
+ * q_out [n][n_q_heads][head_dim]; if kv_out is not NULL the rotated k and v
+ * are also written contiguously to kv_out [2][n][kv_heads][head_dim] (the
+ * prefill attention input).  One launch per layer. */
 int tf_rope_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride, const int32_t* dev_rows,
                       const int32_t* dev_pos, int32_t n, int32_t layer, const void* qkv, int32_t n_q_heads,
-                      const float* inv_freq, void* q_out, void* stream);
+                      const float* inv_freq, void* q_out, void* kv_out, void* stream);
 
 /* Synthetic KV (parity / swap benchmarks): positions [pos_begin,pos_end) of
  * request rid, all layers, value = tf_kv_bits(seed, rid, pos, layer, kv,

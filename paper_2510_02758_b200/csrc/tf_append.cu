@@ -37,7 +37,8 @@ __global__ void append_kernel(PoolView pv, const int32_t* __restrict__ table, in
 __global__ void rope_append_kernel(PoolView pv, const int32_t* __restrict__ table, int32_t stride,
                                    const int32_t* __restrict__ rows, const int32_t* __restrict__ pos, int32_t n,
                                    int32_t layer, const uint16_t* __restrict__ qkv, int32_t hq,
-                                   const float* __restrict__ inv_freq, uint16_t* __restrict__ q_out) {
+                                   const float* __restrict__ inv_freq, uint16_t* __restrict__ q_out,
+                                   uint16_t* __restrict__ kv_out) {
   const int heads = hq + 2 * pv.kv_heads;
   const int warps = blockDim.x / 32;
   const int64_t wid = (int64_t)blockIdx.x * warps + threadIdx.x / 32;
@@ -48,6 +49,7 @@ __global__ void rope_append_kernel(PoolView pv, const int32_t* __restrict__ tabl
   const int p = pos[tok];
   const uint16_t* src = qkv + ((int64_t)tok * heads + h) * D;
   uint16_t* dst;
+  uint16_t* dst2 = nullptr;  // optional contiguous copy of the rotated k / v (prefill attention input)
   bool rotate = true;
   if (h < hq) {
     dst = q_out + ((int64_t)tok * hq + h) * D;
@@ -56,19 +58,21 @@ __global__ void rope_append_kernel(PoolView pv, const int32_t* __restrict__ tabl
     const int blk = table[(int64_t)rows[tok] * stride + p / pv.block_tokens];
     dst = pv.gpu + pv.off(blk, layer, kv, kvh, p % pv.block_tokens);
     rotate = (kv == 0);
+    if (kv_out) dst2 = kv_out + (((int64_t)kv * n + tok) * pv.kv_heads + kvh) * D;
   }
   for (int i = lane; i < D / 2; i += 32) {
     const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 2 * i);
-    if (!rotate) {
-      *reinterpret_cast<uint32_t*>(dst + 2 * i) = w;
-      continue;
+    uint32_t o = w;
+    if (rotate) {
+      const float x1 = __uint_as_float(w << 16), x2 = __uint_as_float(w & 0xFFFF0000u);
+      float sn, cs;
+      sincosf((float)p * inv_freq[i], &sn, &cs);
+      const uint32_t o1 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * cs - x2 * sn));
+      const uint32_t o2 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * sn + x2 * cs));
+      o = o1 | (o2 << 16);
     }
-    const float x1 = __uint_as_float(w << 16), x2 = __uint_as_float(w & 0xFFFF0000u);
-    float sn, cs;
-    sincosf((float)p * inv_freq[i], &sn, &cs);
-    const uint32_t o1 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * cs - x2 * sn));
-    const uint32_t o2 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * sn + x2 * cs));
-    *reinterpret_cast<uint32_t*>(dst + 2 * i) = o1 | (o2 << 16);
+    *reinterpret_cast<uint32_t*>(dst + 2 * i) = o;
+    if (dst2) *reinterpret_cast<uint32_t*>(dst2 + 2 * i) = o;
   }
 }
 
@@ -141,7 +145,7 @@ int tf_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride, con
 
 int tf_rope_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride, const int32_t* dev_rows,
                       const int32_t* dev_pos, int32_t n, int32_t layer, const void* qkv, int32_t n_q_heads,
-                      const float* inv_freq, void* q_out, void* stream) {
+                      const float* inv_freq, void* q_out, void* kv_out, void* stream) {
   Pool* p = get_pool(pool);
   TF_CHECK_ARG(p, "tf_rope_kv_append: unknown pool");
   TF_CHECK_ARG(layer >= 0 && layer < p->n_layers, "tf_rope_kv_append: bad layer %d", layer);
@@ -151,7 +155,7 @@ int tf_rope_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride
   const int64_t warps = (int64_t)n * (n_q_heads + 2 * p->kv_heads);
   rope_append_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       view_of(*p), dev_table, row_stride, dev_rows, dev_pos, n, layer, (const uint16_t*)qkv, n_q_heads, inv_freq,
-      (uint16_t*)q_out);
+      (uint16_t*)q_out, (uint16_t*)kv_out);
   TF_LAUNCH_CHECK();
   return TF_OK;
 }

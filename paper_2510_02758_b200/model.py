@@ -109,17 +109,21 @@ class PagedDecoder:
         meta = torch.tensor([[rid, p0 + i] for rid, t, p0 in seqs for i in range(t.numel())],
                             dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
         rows, pos32 = meta[:, 0].contiguous(), meta[:, 1].contiguous()
-        pos = pos32.long()
         n = toks.numel()
         G = s.n_q_heads // s.n_kv_heads
         x = self.embed[toks]
+        q = torch.empty((n, s.n_q_heads, s.head_dim), device=self.device, dtype=x.dtype)
+        kvb = torch.empty((2, n, s.n_kv_heads, s.head_dim), device=self.device, dtype=x.dtype)
+        k, v = kvb[0], kvb[1]
         for li, L in enumerate(self.layers):
             h = self._rms(x, L["ln1"])
-            qkv = (h @ L["wqkv"]).view(n, s.n_q_heads + 2 * s.n_kv_heads, s.head_dim)
-            q = self._rope(qkv[:, : s.n_q_heads], pos)
-            k = self._rope(qkv[:, s.n_q_heads: s.n_q_heads + s.n_kv_heads], pos).contiguous()
-            v = qkv[:, s.n_q_heads + s.n_kv_heads:].contiguous()
-            self._append(dp, rows, pos32, li, k.view(n, -1), v.view(n, -1), st)
+            qkv = h @ L["wqkv"]
+            # rotary q/k + paged K/V append + contiguous k/v for the prompt attention
+            check(lib.tf_rope_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb,
+                                        C.c_void_p(rows.data_ptr()), C.c_void_p(pos32.data_ptr()), n, li,
+                                        C.c_void_p(qkv.data_ptr()), s.n_q_heads, C.c_void_p(self._inv_freq.data_ptr()),
+                                        C.c_void_p(q.data_ptr()), C.c_void_p(kvb.data_ptr()),
+                                        C.c_void_p(st.cuda_stream)), "tf_rope_kv_append")
             outs, o = [], 0
             with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION]):
                 for ln in lens:
@@ -311,7 +315,8 @@ class PagedDecoder:
             check(lib.tf_rope_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb,
                                         C.c_void_p(rows.data_ptr()), C.c_void_p(pos32.data_ptr()), B, li,
                                         C.c_void_p(qkv.data_ptr()), s.n_q_heads, C.c_void_p(self._inv_freq.data_ptr()),
-                                        C.c_void_p(q.data_ptr()), C.c_void_p(st.cuda_stream)), "tf_rope_kv_append")
+                                        C.c_void_p(q.data_ptr()), None, C.c_void_p(st.cuda_stream)),
+                  "tf_rope_kv_append")
             if timing is not None:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)

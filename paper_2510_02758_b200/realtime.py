@@ -47,6 +47,7 @@ class RealtimeEngine(Engine):
         self.on_step = on_step  # callback(record dict) after every decode iteration
         self.max_steps = max_steps
         self.steps = []  # per decode iteration: start, end, batch size, produced, effective weight
+        self.jobs = []  # every GPU job (decode and prefill): (kind, start, end, device seconds)
         self._gpu = None  # (kind, payload, start_time, end_event)
         self._lanes = {"d2h": None, "h2d": None}  # (start_time, end_event)
         self._anchor = None
@@ -140,6 +141,7 @@ class RealtimeEngine(Engine):
                 kind, payload, start, _ = self._gpu
                 self._gpu = None
                 dur = max(t - start, 1e-9)
+                self.jobs.append((kind, start, t, dur))
                 if kind == "prefill":
                     self._on_prefill_done(t, min(payload.members), payload, dur)
                 else:
