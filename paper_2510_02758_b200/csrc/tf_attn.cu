@@ -550,11 +550,245 @@ __global__ void __launch_bounds__((kConsumers + 1) * 32) paged_attn_tma_kernel(c
   }
 }
 
+// ------------------------------------------------------------------------
+// v3: tensor cores for QK and PV (mma.sync m16n8k16 bf16 -> fp32).
+// Each warp owns every 4th block of the CTA's split and streams it through a
+// private 3-stage cp.async ring in shared memory (K and V tiles, rows padded
+// to 272 B so ldmatrix is conflict-free).  Per 16-token block a warp issues
+// 16 MMAs for S = Q K^T (the G q heads of the kv head fill rows 0..G-1 of
+// the 16-row A tile) and 16 MMAs for O += P V, where P is re-used straight
+// from the S accumulators as the A operand (no shuffle / smem round trip).
+// ~100 instructions per block per warp instead of ~1000 on the CUDA cores.
+constexpr int kV3Warps = 4;
+constexpr int kV3Stages = 3;
+constexpr int kRowPad = 136;  // bf16 elements per padded smem row (128 + 8)
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void mma_bf16(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(lo)) |
+         ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(hi)) << 16);
+}
+
+template <int G>
+__global__ void __launch_bounds__(kV3Warps * 32, 2) paged_attn_mma_kernel(const AttnArgs a) {
+  constexpr int D = 128;
+  static_assert(G >= 1 && G <= 8, "v3 packs the group into rows 0..7 of the 16-row tile");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // per warp: [kV3Stages][K|V][16 rows][kRowPad]
+  constexpr int kTileElems = kBlk * kRowPad;
+  constexpr int kWarpElems = kV3Stages * 2 * kTileElems;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw) + warp * kWarpElems;
+
+  const int bh = blockIdx.y;
+  const int b = bh / a.kv_heads, kvh = bh % a.kv_heads;
+  const int split = blockIdx.x;
+  const int ctx = a.ctx[b];
+  const int nblk = (ctx + kBlk - 1) / kBlk;
+  const int blk_lo = split * a.blocks_per_split;
+  const int blk_hi = min(nblk, blk_lo + a.blocks_per_split);
+  const int nmine = blk_hi > blk_lo + warp ? (blk_hi - blk_lo - warp + kV3Warps - 1) / kV3Warps : 0;
+
+  const int64_t tile = (int64_t)kBlk * D;
+  const int64_t koff = (((int64_t)a.layer * 2 + 0) * a.kv_heads + kvh) * tile;
+  const int64_t voff = (((int64_t)a.layer * 2 + 1) * a.kv_heads + kvh) * tile;
+  const int32_t* trow = a.table + (int64_t)a.rows[b] * a.stride;
+
+  auto issue = [&](int j) {  // warp-local block j -> stage j % kV3Stages
+    if (j < nmine) {
+      const int blk = blk_lo + warp + j * kV3Warps;
+      const int64_t base = (int64_t)__ldg(trow + blk) * a.block_elems;
+      uint16_t* ks = ring + (j % kV3Stages) * 2 * kTileElems;
+      uint16_t* vs = ks + kTileElems;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {  // 256 x 16 B per tile, 8 per lane
+        const int ch = u * 32 + lane;
+        const int r = ch >> 4, c16 = ch & 15;
+        cp_async16(ks + r * kRowPad + c16 * 8, a.pool + base + koff + ch * 8);
+        cp_async16(vs + r * kRowPad + c16 * 8, a.pool + base + voff + ch * 8);
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+
+  // Q as the A operand: rows 0..G-1 = the group's heads (scaled later), rest 0
+  const int r0 = lane >> 2, cq = (lane & 3) * 2;
+  uint32_t qa[8][4];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    uint32_t lo = 0, hi = 0;
+    if (r0 < G) {
+      const uint16_t* qrow = a.q + ((int64_t)b * a.hq + kvh * G + r0) * D + kk * 16 + cq;
+      lo = *reinterpret_cast<const uint32_t*>(qrow);
+      hi = *reinterpret_cast<const uint32_t*>(qrow + 8);
+    }
+    qa[kk][0] = lo;
+    qa[kk][1] = 0;  // row r0 + 8 >= 8 > G - 1
+    qa[kk][2] = hi;
+    qa[kk][3] = 0;
+  }
+  float o[16][4];
+#pragma unroll
+  for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m0 = -FLT_MAX, l0 = 0.f;  // row r0 (rows r0+8 are padding)
+
+  for (int j = 0; j < nmine; ++j) {
+    issue(j + 2);
+    cp_async_wait<2>();
+    __syncwarp();
+    const uint16_t* ks = ring + (j % kV3Stages) * 2 * kTileElems;
+    const uint16_t* vs = ks + kTileElems;
+    const int blk = blk_lo + warp + j * kV3Warps;
+    // ---- S = Q K^T : two n-tiles of 8 tokens, 8 k-steps of 16 dims
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row within matrix, matrix id
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t b00, b01, b10, b11;
+      // matrices: (tok 0-7, dims lo), (tok 0-7, dims hi), (tok 8-15, dims lo), (tok 8-15, dims hi)
+      const uint16_t* p = ks + ((lm >> 1) * 8 + lr) * kRowPad + kk * 16 + (lm & 1) * 8;
+      ldsm_x4(b00, b01, b10, b11, p);
+      mma_bf16(s[0], qa[kk], b00, b01);
+      mma_bf16(s[1], qa[kk], b10, b11);
+    }
+    // ---- online softmax on row r0 (c0, c1 of each n-tile)
+    float mx = -FLT_MAX;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = nt * 8 + cq + e;
+        float v = s[nt][e] * a.scale_log2;
+        if (blk * kBlk + t >= ctx) v = -FLT_MAX;
+        s[nt][e] = v;
+        mx = fmaxf(mx, v);
+      }
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mn = fmaxf(m0, mx);
+    const float alpha = exp2f(m0 - mn);
+    m0 = mn;
+    float ps = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float p = s[nt][e] > -FLT_MAX ? exp2f(s[nt][e] - mn) : 0.f;
+        s[nt][e] = p;
+        ps += p;
+      }
+    }
+    l0 = l0 * alpha + ps;
+#pragma unroll
+    for (int n = 0; n < 16; ++n) {
+      o[n][0] *= alpha;
+      o[n][1] *= alpha;
+    }
+    // ---- O += P V : P from the S accumulators (rows r0 / r0+8 = 0), V via ldmatrix.trans
+    uint32_t pa[4];
+    pa[0] = pack_bf16(s[0][0], s[0][1]);
+    pa[1] = 0;
+    pa[2] = pack_bf16(s[1][0], s[1][1]);
+    pa[3] = 0;
+    const int valid = ctx - blk * kBlk;
+    if (valid < kBlk) {
+      // V slots past ctx may hold stale bits (NaN * 0 = NaN in the MMA): zero them
+      uint16_t* vw = const_cast<uint16_t*>(vs);
+      for (int e = lane; e < (kBlk - valid) * (D / 8); e += 32) {
+        const int r = valid + e / (D / 8), c8 = e % (D / 8);
+        *reinterpret_cast<uint4*>(vw + r * kRowPad + c8 * 8) = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int np = 0; np < 8; ++np) {  // pairs of 8-dim n-tiles
+      uint32_t v0, v1, v2, v3;
+      // matrices: (tok 0-7, dims 16np..+8), (tok 8-15, same), (tok 0-7, dims +8), (tok 8-15, dims +8)
+      const uint16_t* p = vs + ((lm & 1) * 8 + lr) * kRowPad + np * 16 + (lm >> 1) * 8;
+      ldsm_x4_t(v0, v1, v2, v3, p);
+      mma_bf16(o[2 * np], pa, v0, v1);
+      mma_bf16(o[2 * np + 1], pa, v2, v3);
+    }
+    __syncwarp();  // the stage is refilled by issue(j + 3) next iteration
+  }
+  cp_async_wait<0>();
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+
+  // ---- merge the 4 warps (reuse the ring memory), write split / output
+  __syncthreads();
+  float* acc_sh = reinterpret_cast<float*>(smem_raw);  // [kV3Warps][G][D]
+  __shared__ float m_sh[kV3Warps][8], l_sh[kV3Warps][8];
+  if (r0 < G) {
+#pragma unroll
+    for (int n = 0; n < 16; ++n) {
+      acc_sh[(warp * G + r0) * D + n * 8 + cq] = o[n][0];
+      acc_sh[(warp * G + r0) * D + n * 8 + cq + 1] = o[n][1];
+    }
+    if ((lane & 3) == 0) {
+      m_sh[warp][r0] = m0;
+      l_sh[warp][r0] = l0;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
+    const int g = e / D, d = e % D;
+    float mm = -FLT_MAX;
+#pragma unroll
+    for (int w = 0; w < kV3Warps; ++w) mm = fmaxf(mm, m_sh[w][g]);
+    float ll = 0.f, aa = 0.f;
+#pragma unroll
+    for (int w = 0; w < kV3Warps; ++w) {
+      const float f = (m_sh[w][g] == -FLT_MAX) ? 0.f : exp2f(m_sh[w][g] - mm);
+      ll += l_sh[w][g] * f;
+      aa += acc_sh[(w * G + g) * D + d] * f;
+    }
+    const int64_t row = (int64_t)b * a.hq + kvh * G + g;
+    if (a.splits == 1) {
+      a.out[row * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(ll > 0.f ? aa / ll : 0.f));
+    } else {
+      a.ws_acc[(row * a.splits + split) * D + d] = aa;
+      if (d == 0) {
+        a.ws_ml[(row * a.splits + split) * 2 + 0] = mm;
+        a.ws_ml[(row * a.splits + split) * 2 + 1] = ll;
+      }
+    }
+  }
+}
+
 static int attn_impl() {
   static int impl = -1;
   if (impl < 0) {
     const char* e = getenv("TF_ATTN_IMPL");
-    impl = (e && e[0] == '1') ? 1 : 2;
+    impl = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 3;
   }
   return impl;
 }
@@ -564,7 +798,7 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
   const int base = std::max(1, B * kv_heads);
   // >= ~4 waves of resident CTAs (3 per SM) so the tail wave is cheap,
   // >= 8 blocks per split so the pipeline prologue is amortised
-  const int target = attn_impl() == 2 ? 148 * 3 * 4 : 148 * 6;
+  const int target = attn_impl() >= 2 ? 148 * 2 * 4 : 148 * 6;  // v2/v3 run 2 CTAs per SM
   int s = std::max(1, std::min((target + base - 1) / base, (nblk + 7) / 8));
   int per = (nblk + s - 1) / s;
   s = (nblk + per - 1) / per;
@@ -575,7 +809,16 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
 template <int D, int G>
 static int launch(const AttnArgs& a, int B, cudaStream_t st) {
   dim3 grid(a.splits, B * a.kv_heads);
-  if (attn_impl() == 2) {
+  if (attn_impl() == 3 && D == 128 && G <= 8) {
+    const int smem = kV3Warps * kV3Stages * 2 * kBlk * kRowPad * 2;
+    static bool attr3 = false;
+    if (!attr3) {
+      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<(G <= 8 ? G : 8)>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr3 = true;
+    }
+    paged_attn_mma_kernel<(G <= 8 ? G : 8)><<<grid, kV3Warps * 32, smem, st>>>(a);
+  } else if (attn_impl() >= 2) {
     const int smem = kStages * 2 * kBlk * D * 2;
     static bool attr = false;
     if (!attr) {
