@@ -114,6 +114,16 @@ int tf_rope_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride
                       const int32_t* dev_pos, int32_t n, int32_t layer, const void* qkv, int32_t n_q_heads,
                       const float* inv_freq, void* q_out, void* kv_out, void* stream);
 
+/* Same as tf_rope_kv_append for decode, with the write-through fused into
+ * the epilogue (reference write-through: engine.py:781-813):
+ * when dev_host_table[rows[i]][pos[i]/block] >= 0 the appended k/v are also
+ * stored into that block of the pinned host store (same slot, same layout),
+ * so a token's KV is mirrored to the host in the step that makes it
+ * (prefill or decode).  kv_out as in tf_rope_kv_append (may be NULL). */
+int tf_rope_kv_append_wt(int64_t pool, const int32_t* dev_table, const int32_t* dev_host_table, int32_t row_stride,
+                         const int32_t* dev_rows, const int32_t* dev_pos, int32_t n, int32_t layer, const void* qkv,
+                         int32_t n_q_heads, const float* inv_freq, void* q_out, void* kv_out, void* stream);
+
 /* Synthetic KV (parity / swap benchmarks): positions [pos_begin,pos_end) of
  * request rid, all layers, value = tf_kv_bits(seed, rid, pos, layer, kv,
  * head, dim) (identical to oracle/dataplane.py kv_bits). */

@@ -98,6 +98,7 @@ SIGNATURES = {
     "tf_kv_scatter_h2d": (C.c_int, [_I64, C.POINTER(TfSeg), _I32, _I32, _I32, _I32, _P]),
     "tf_kv_append": (C.c_int, [_I64, _P, _I32, _P, _P, _I32, _I32, _P, _P, _I64, _P]),
     "tf_rope_kv_append": (C.c_int, [_I64, _P, _I32, _P, _P, _I32, _I32, _P, _I32, _P, _P, _P, _P]),
+    "tf_rope_kv_append_wt": (C.c_int, [_I64, _P, _P, _I32, _P, _P, _I32, _I32, _P, _I32, _P, _P, _P, _P]),
     "tf_kv_fill_synthetic": (C.c_int, [_I64, _P, _I32, C.POINTER(TfSpan), _I32, C.c_uint32, _P]),
     "tf_q_fill_synthetic": (C.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, C.c_uint32, _P]),
     "tf_paged_decode_attn": (C.c_int, [_I64, _P, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, C.c_float, _P, _P,

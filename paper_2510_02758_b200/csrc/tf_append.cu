@@ -38,7 +38,7 @@ __global__ void rope_append_kernel(PoolView pv, const int32_t* __restrict__ tabl
                                    const int32_t* __restrict__ rows, const int32_t* __restrict__ pos, int32_t n,
                                    int32_t layer, const uint16_t* __restrict__ qkv, int32_t hq,
                                    const float* __restrict__ inv_freq, uint16_t* __restrict__ q_out,
-                                   uint16_t* __restrict__ kv_out) {
+                                   uint16_t* __restrict__ kv_out, const int32_t* __restrict__ host_table) {
   const int heads = hq + 2 * pv.kv_heads;
   const int warps = blockDim.x / 32;
   const int64_t wid = (int64_t)blockIdx.x * warps + threadIdx.x / 32;
@@ -50,6 +50,7 @@ __global__ void rope_append_kernel(PoolView pv, const int32_t* __restrict__ tabl
   const uint16_t* src = qkv + ((int64_t)tok * heads + h) * D;
   uint16_t* dst;
   uint16_t* dst2 = nullptr;  // optional contiguous copy of the rotated k / v (prefill attention input)
+  uint16_t* dst3 = nullptr;  // optional host-store slot (fused write-through)
   bool rotate = true;
   if (h < hq) {
     dst = q_out + ((int64_t)tok * hq + h) * D;
@@ -59,6 +60,12 @@ __global__ void rope_append_kernel(PoolView pv, const int32_t* __restrict__ tabl
     dst = pv.gpu + pv.off(blk, layer, kv, kvh, p % pv.block_tokens);
     rotate = (kv == 0);
     if (kv_out) dst2 = kv_out + (((int64_t)kv * n + tok) * pv.kv_heads + kvh) * D;
+    if (host_table) {
+      // fused write-through: the same slot of the request's host block, written
+      // straight over PCIe into the mapped pinned store (posted writes)
+      const int hb = host_table[(int64_t)rows[tok] * stride + p / pv.block_tokens];
+      if (hb >= 0) dst3 = pv.host + pv.off(hb, layer, kv, kvh, p % pv.block_tokens);
+    }
   }
   for (int i = lane; i < D / 2; i += 32) {
     const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 2 * i);
@@ -73,6 +80,7 @@ __global__ void rope_append_kernel(PoolView pv, const int32_t* __restrict__ tabl
     }
     *reinterpret_cast<uint32_t*>(dst + 2 * i) = o;
     if (dst2) *reinterpret_cast<uint32_t*>(dst2 + 2 * i) = o;
+    if (dst3) *reinterpret_cast<uint32_t*>(dst3 + 2 * i) = o;
   }
 }
 
@@ -155,7 +163,26 @@ int tf_rope_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride
   const int64_t warps = (int64_t)n * (n_q_heads + 2 * p->kv_heads);
   rope_append_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       view_of(*p), dev_table, row_stride, dev_rows, dev_pos, n, layer, (const uint16_t*)qkv, n_q_heads, inv_freq,
-      (uint16_t*)q_out, (uint16_t*)kv_out);
+      (uint16_t*)q_out, (uint16_t*)kv_out, nullptr);
+  TF_LAUNCH_CHECK();
+  return TF_OK;
+}
+
+int tf_rope_kv_append_wt(int64_t pool, const int32_t* dev_table, const int32_t* dev_host_table, int32_t row_stride,
+                         const int32_t* dev_rows, const int32_t* dev_pos, int32_t n, int32_t layer, const void* qkv,
+                         int32_t n_q_heads, const float* inv_freq, void* q_out, void* kv_out, void* stream) {
+  Pool* p = get_pool(pool);
+  TF_CHECK_ARG(p, "tf_rope_kv_append_wt: unknown pool");
+  TF_CHECK_ARG(p->host_dev, "tf_rope_kv_append_wt: pool has no host tier");
+  TF_CHECK_ARG(layer >= 0 && layer < p->n_layers, "tf_rope_kv_append_wt: bad layer %d", layer);
+  TF_CHECK_ARG(n >= 0, "tf_rope_kv_append_wt: n < 0");
+  if (n == 0) return TF_OK;
+  TF_CHECK_ARG(dev_table && dev_host_table && dev_rows && dev_pos && qkv && inv_freq && q_out,
+               "tf_rope_kv_append_wt: NULL pointer");
+  const int64_t warps = (int64_t)n * (n_q_heads + 2 * p->kv_heads);
+  rope_append_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      view_of(*p), dev_table, row_stride, dev_rows, dev_pos, n, layer, (const uint16_t*)qkv, n_q_heads, inv_freq,
+      (uint16_t*)q_out, (uint16_t*)kv_out, dev_host_table);
   TF_LAUNCH_CHECK();
   return TF_OK;
 }

@@ -40,8 +40,8 @@ import torch
 from . import _lib
 from ._lib import TIER_GPU, TIER_HOST, TfSeg, TfSpan, check, lib
 
-LIVE, DETACHED, RESERVED = np.uint8(1), np.uint8(2), np.uint8(4)
-CLR_LIVE, CLR_DETACHED, CLR_RESERVED = np.uint8(0xFE), np.uint8(0xFD), np.uint8(0xFB)
+LIVE, DETACHED, RESERVED, HOSTV = np.uint8(1), np.uint8(2), np.uint8(4), np.uint8(8)
+CLR_LIVE, CLR_DETACHED, CLR_RESERVED, CLR_HOSTV = np.uint8(0xFE), np.uint8(0xFD), np.uint8(0xFB), np.uint8(0xF7)
 
 
 def _i32(a) -> C.Array:
@@ -122,6 +122,11 @@ class GpuDataPlane:
         self.table = torch.full((n_rows + 1, self.nlb), -1, dtype=torch.int32, device=dev)
         self.scratch_row = n_rows
         self.scratch_block = None
+        # fused write-through (realtime): device host-block table read by the
+        # decode epilogue; HOSTV flags mark positions mirrored on the host
+        self.fused_wt = False
+        self.htable = None
+        self._pending_htable = []
         if mode == "replay":
             self.s_compute = self.s_evict = self.s_load = torch.cuda.Stream(device=dev)
         else:
@@ -141,6 +146,14 @@ class GpuDataPlane:
         ws = max(1, int(lib.tf_paged_decode_attn_workspace(pool.handle, max(1, len(reqs)), self.max_len, 64)))
         self._attn_ws = torch.empty(ws, dtype=torch.uint8, device=dev)
         self.attn_out = None
+
+    def enable_fused_write_through(self):
+        """Mirror every decoded token to the host inside the decode step
+        (SURVEY 8f #1) instead of in separate write-through chunks."""
+        if self.mode != "realtime":
+            raise ValueError("fused write-through changes the token-count semantics; realtime mode only")
+        self.fused_wt = True
+        self.htable = torch.full_like(self.table, -1)
 
     def enable_scratch(self):
         """Reserve one block for the padding rows of captured decode graphs."""
@@ -257,11 +270,19 @@ class GpuDataPlane:
                 raise _lib.InvariantError(f"prefill of {rid} overlaps resident KV")
             f[lo:hi] |= RESERVED
             self._reconcile(rid, range(lo // self.B, (hi - 1) // self.B + 1))
+            if self.fused_wt:
+                htab = self.htab[rid]
+                for j in range(lo // self.B, (hi - 1) // self.B + 1):
+                    if htab[j] < 0:
+                        htab[j] = self.pool.alloc(TIER_HOST, 1)[0]
+                        self._pending_htable.append((rid, j, int(htab[j])))
             spans.append((rid, lo, hi))
             self.stats["fill_tokens"] += hi - lo
         self._wait_d2h_of(spans, self.s_compute)
         if self.model is not None and self.kv_source == "model":
             self._flush_table(self.s_compute)
+            if self.fused_wt:
+                self._flush_htable(self.s_compute)
             self.model.prefill(self, job, spans, eng)
         else:
             self._write_kv(spans, self.s_compute)
@@ -269,7 +290,13 @@ class GpuDataPlane:
     def fill_done(self, rid):
         f = self.flags[rid]
         m = (f & RESERVED) != 0
-        f[m] = (f[m] & CLR_RESERVED) | LIVE
+        if self.fused_wt:
+            idx = np.nonzero(m)[0]
+            f[m] = (f[m] & CLR_RESERVED) | LIVE | HOSTV
+            if len(idx):
+                self.host_hi[rid] = max(self.host_hi[rid], int(idx[-1]) + 1)
+        else:
+            f[m] = (f[m] & CLR_RESERVED) | LIVE
         if self.model is not None and self.kv_source == "model":
             self.model.fill_commit(rid)
 
@@ -284,12 +311,19 @@ class GpuDataPlane:
             self._appending[rid] = p
             if p % self.B == 0 or self.gtab[rid][p // self.B] < 0:
                 self._reconcile(rid, [p // self.B])
+            if self.fused_wt:
+                j = p // self.B
+                if self.htab[rid][j] < 0:
+                    self.htab[rid][j] = self.pool.alloc(TIER_HOST, 1)[0]
+                    self._pending_htable.append((rid, j, int(self.htab[rid][j])))
             spans.append((rid, p, p + 1))
         self.stats["append_tokens"] += len(batch)
         self.stats["decode_steps"] += 1
         self._wait_d2h_of(spans, self.s_compute)
         if self.model is not None and self.kv_source == "model":
             self._flush_table(self.s_compute)
+            if self.fused_wt:
+                self._flush_htable(self.s_compute)
             self.model.decode(self, batch, eng)
         else:
             self._write_kv(spans, self.s_compute)
@@ -302,6 +336,9 @@ class GpuDataPlane:
         for rid in batch:
             f = self.flags[rid]
             p = self._appending.pop(rid)  # the one position this step reserved
+            if self.fused_wt and rid in made:
+                f[p] |= HOSTV  # mirrored to the host by the fused epilogue
+                self.host_hi[rid] = max(self.host_hi[rid], p + 1)
             if rid in made:
                 f[p] = (f[p] & CLR_RESERVED) | LIVE
             else:
@@ -343,6 +380,8 @@ class GpuDataPlane:
     def d2h_done(self, ch, alive):
         rid, lo, hi, kind, ev = self._d2h_busy
         self._d2h_busy = None
+        if self.fused_wt and alive:
+            self.flags[rid][lo:hi] |= HOSTV
         if kind == "evict":
             self.flags[rid][lo:hi] &= CLR_DETACHED
             if self.mode == "realtime":
@@ -396,9 +435,32 @@ class GpuDataPlane:
     def drop_host(self, rid):
         tab = self.htab[rid]
         ids = [int(b) for b in tab if b >= 0]
+        if self.fused_wt:
+            for j in np.nonzero(tab >= 0)[0]:
+                self._pending_htable.append((rid, int(j), -1))
+            self.flags[rid] &= CLR_HOSTV
         tab[:] = -1
         self.pool.free(TIER_HOST, ids)
         self.host_hi[rid] = 0
+
+    def host_frontier(self, rid, cs, total):
+        """Fused write-through: the host prefix extends over every position the
+        decode epilogue (or a landed chunk) already mirrored."""
+        f = self.flags[rid]
+        while cs < total and f[cs] & HOSTV:
+            cs += 1
+        return cs
+
+    def _flush_htable(self, stream):
+        if not self._pending_htable:
+            return
+        last = {}
+        for row, lb, blk in self._pending_htable:
+            last[(row, lb)] = blk
+        self._pending_htable = []
+        t = np.asarray([(r, j, b) for (r, j), b in last.items()], np.int32).reshape(-1)
+        check(lib.tf_table_apply(C.c_void_p(self.htable.data_ptr()), self.nlb, _i32(t), len(t) // 3,
+                                 C.c_void_p(stream.cuda_stream)), "tf_table_apply(host)")
 
     def finish(self, rid):
         f = self.flags[rid]

@@ -118,12 +118,22 @@ class PagedDecoder:
         for li, L in enumerate(self.layers):
             h = self._rms(x, L["ln1"])
             qkv = h @ L["wqkv"]
-            # rotary q/k + paged K/V append + contiguous k/v for the prompt attention
-            check(lib.tf_rope_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb,
-                                        C.c_void_p(rows.data_ptr()), C.c_void_p(pos32.data_ptr()), n, li,
-                                        C.c_void_p(qkv.data_ptr()), s.n_q_heads, C.c_void_p(self._inv_freq.data_ptr()),
-                                        C.c_void_p(q.data_ptr()), C.c_void_p(kvb.data_ptr()),
-                                        C.c_void_p(st.cuda_stream)), "tf_rope_kv_append")
+            # rotary q/k + paged K/V append (+ host mirror when write-through is
+            # fused) + contiguous k/v for the prompt attention
+            if getattr(dp, "fused_wt", False):
+                check(lib.tf_rope_kv_append_wt(dp.pool.handle, C.c_void_p(dp.table.data_ptr()),
+                                               C.c_void_p(dp.htable.data_ptr()), dp.nlb, C.c_void_p(rows.data_ptr()),
+                                               C.c_void_p(pos32.data_ptr()), n, li, C.c_void_p(qkv.data_ptr()),
+                                               s.n_q_heads, C.c_void_p(self._inv_freq.data_ptr()),
+                                               C.c_void_p(q.data_ptr()), C.c_void_p(kvb.data_ptr()),
+                                               C.c_void_p(st.cuda_stream)), "tf_rope_kv_append_wt")
+            else:
+                check(lib.tf_rope_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb,
+                                            C.c_void_p(rows.data_ptr()), C.c_void_p(pos32.data_ptr()), n, li,
+                                            C.c_void_p(qkv.data_ptr()), s.n_q_heads,
+                                            C.c_void_p(self._inv_freq.data_ptr()), C.c_void_p(q.data_ptr()),
+                                            C.c_void_p(kvb.data_ptr()), C.c_void_p(st.cuda_stream)),
+                      "tf_rope_kv_append")
             outs, o = [], 0
             with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION]):
                 for ln in lens:
@@ -312,11 +322,20 @@ class PagedDecoder:
             h = self._rms(x, L["ln1"])
             qkv = h @ L["wqkv"]
             # fused rotary embedding + paged K/V append + q layout (one launch)
-            check(lib.tf_rope_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb,
-                                        C.c_void_p(rows.data_ptr()), C.c_void_p(pos32.data_ptr()), B, li,
-                                        C.c_void_p(qkv.data_ptr()), s.n_q_heads, C.c_void_p(self._inv_freq.data_ptr()),
-                                        C.c_void_p(q.data_ptr()), None, C.c_void_p(st.cuda_stream)),
-                  "tf_rope_kv_append")
+            if getattr(dp, "fused_wt", False):
+                # write-through fused into the append epilogue (host mirror in the same step)
+                check(lib.tf_rope_kv_append_wt(dp.pool.handle, C.c_void_p(dp.table.data_ptr()),
+                                               C.c_void_p(dp.htable.data_ptr()), dp.nlb, C.c_void_p(rows.data_ptr()),
+                                               C.c_void_p(pos32.data_ptr()), B, li, C.c_void_p(qkv.data_ptr()),
+                                               s.n_q_heads, C.c_void_p(self._inv_freq.data_ptr()),
+                                               C.c_void_p(q.data_ptr()), None, C.c_void_p(st.cuda_stream)),
+                      "tf_rope_kv_append_wt")
+            else:
+                check(lib.tf_rope_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb,
+                                            C.c_void_p(rows.data_ptr()), C.c_void_p(pos32.data_ptr()), B, li,
+                                            C.c_void_p(qkv.data_ptr()), s.n_q_heads,
+                                            C.c_void_p(self._inv_freq.data_ptr()), C.c_void_p(q.data_ptr()), None,
+                                            C.c_void_p(st.cuda_stream)), "tf_rope_kv_append")
             if timing is not None:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)

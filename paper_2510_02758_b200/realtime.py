@@ -55,6 +55,19 @@ class RealtimeEngine(Engine):
         self.wall_s = 0.0
         self._stop = False
 
+    # ------------------------------------------------- fused write-through
+    def _after_decode_commit(self, produced):
+        if not self.dp.fused_wt:
+            return
+        for rid in produced:
+            kv = self.state[rid].kv
+            kv.cpu_synced = self.dp.host_frontier(rid, kv.cpu_synced, kv.total_kv)
+
+    def _after_d2h_land(self, rid):
+        if self.dp.fused_wt:
+            kv = self.state[rid].kv
+            kv.cpu_synced = self.dp.host_frontier(rid, kv.cpu_synced, kv.total_kv)
+
     # ------------------------------------------------------------------ clock
     def _clock(self) -> float:
         return time.perf_counter() - self._t0 + self.skipped_s

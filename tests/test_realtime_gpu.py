@@ -9,7 +9,7 @@ from conftest import load_golden, pool_blocks, trace_path
 pytestmark = pytest.mark.gpu
 
 
-def _run(cuda, name="c1_tokenflow", engine=0, max_steps=None, graphs=False):
+def _run(cuda, name="c1_tokenflow", engine=0, max_steps=None, graphs=False, fused=False):
     from paper_2510_02758_b200 import configs
     from paper_2510_02758_b200.costs import CostModel
     from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
@@ -27,6 +27,8 @@ def _run(cuda, name="c1_tokenflow", engine=0, max_steps=None, graphs=False):
     model = PagedDecoder(shape, device=cuda)
     dp = GpuDataPlane(tr.requests, pool, mode="realtime", kv_source="model", model=model,
                       n_q_heads=shape.n_q_heads, engine=engine)
+    if fused:
+        dp.enable_fused_write_through()
     if graphs:
         dp.enable_scratch()
         model.enable_graphs(dp, buckets=(2, 4, 8))
@@ -36,9 +38,14 @@ def _run(cuda, name="c1_tokenflow", engine=0, max_steps=None, graphs=False):
     return g, eng, res, dp, model
 
 
-@pytest.mark.parametrize("engine,graphs", [(0, False), (1, False), (1, True)])
-def test_realtime_c1_completes_with_invariants(cuda, engine, graphs):
-    g, eng, res, dp, model = _run(cuda, engine=engine, graphs=graphs)
+@pytest.mark.parametrize("engine,graphs,fused", [(0, False, False), (1, False, False), (2, True, False),
+                                                 (2, True, True)])
+def test_realtime_c1_completes_with_invariants(cuda, engine, graphs, fused):
+    g, eng, res, dp, model = _run(cuda, engine=engine, graphs=graphs, fused=fused)
+    if fused:
+        # decoded / prefilled tokens are mirrored in their own step: almost no
+        # write-through chunks, preemptions release everything instantly
+        assert dp.stats["d2h_launches"] < 0.2 * dp.stats["decode_steps"]
     eng._final_invariants(res.records)
     assert all(len(r.gen_times) == r.output_len for r in res.records)
     assert res.total_preemptions > 0 and dp.stats["h2d_tokens"] > 0 and dp.stats["d2h_tokens"] > 0
