@@ -361,6 +361,15 @@ def main():
     args = ap.parse_args()
     if args.host_blocks <= 0:
         args.host_blocks = 26000 if args.full_run else 16384
+        # never pin more than ~60% of the host's available RAM across the
+        # node's ranks (one pinned host tier per GPU replica)
+        try:
+            avail_kb = next(int(line.split()[1]) for line in open("/proc/meminfo") if line.startswith("MemAvailable"))
+            world = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1"))))
+            cap = int(avail_kb * 1024 * 0.6 / world / (2 << 20))
+            args.host_blocks = max(1024, min(args.host_blocks, cap))
+        except (OSError, StopIteration, ValueError):
+            pass
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     if args.impl == "reference":

@@ -167,7 +167,8 @@ class GpuDataPlane:
     def _reconcile(self, rid, blocks):
         f, tab = self.flags[rid], self.gtab[rid]
         blocks = sorted(set(int(j) for j in blocks))
-        occ = [bool(f[j * self.B:(j + 1) * self.B].any()) for j in blocks]
+        # HBM occupancy = LIVE | DETACHED | RESERVED (HOSTV only marks the host mirror)
+        occ = [bool((f[j * self.B:(j + 1) * self.B] & 7).any()) for j in blocks]
         freed = []
         for j, o in zip(blocks, occ):
             if not o and tab[j] >= 0:
