@@ -149,18 +149,37 @@ def run_ours(args):
     world, rank, local = _dist()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    tp_mode = args.config == "c4"
+    tp = lockstep = None
     if world > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    c2 = configs.C2
+    if tp_mode:
+        # C4: one model over all ranks (TP = world), NCCL all-reduces on the
+        # data path, completion/clock consensus over a CPU group on the control path
+        from paper_2510_02758_b200.tp import Lockstep, TpGroup
+
+        tp = TpGroup(rank, world)
+        if world > 1:
+            import torch.distributed as dist
+
+            lockstep = Lockstep(dist.new_group(backend="gloo"))
+        c2 = configs.c4(world)
+        tr = _trace_for_rank(0, 1, args.arrivals)
+        if world > 1 and args.graphs:
+            args.graphs = 0  # eager decode under TP: NCCL all-reduces are not captured in graphs
+    else:
+        c2 = configs.C2
+        tr = _trace_for_rank(rank, world, args.arrivals)
     shape = c2.model
-    tr = _trace_for_rank(rank, world, args.arrivals)
+    tp_size = world if tp_mode else 1
     n_blocks = math.ceil(c2.gpu_mem_tokens / 16) + 4 * len(tr.requests) + c2.max_batch + 1
-    pool = KvPool(n_blocks, args.host_blocks, shape.n_layers, shape.n_kv_heads, shape.head_dim, device=dev)
-    model = PagedDecoder(shape, device=dev, seed=rank)
+    pool = KvPool(n_blocks, args.host_blocks, shape.n_layers, shape.n_kv_heads // tp_size, shape.head_dim,
+                  device=dev)
+    model = PagedDecoder(shape, device=dev, seed=0 if tp_mode else rank, tp=tp)
     dp = GpuDataPlane(tr.requests, pool, mode="realtime", kv_source="model", model=model,
-                      n_q_heads=shape.n_q_heads, engine=args.swap_engine)
+                      n_q_heads=shape.n_q_heads // tp_size, engine=args.swap_engine)
     if args.fused_wt:
         dp.enable_fused_write_through()
     if args.graphs:
@@ -197,7 +216,7 @@ def run_ours(args):
                 if not args.full_run:
                     eng._stop = True
 
-    eng = RealtimeEngine(tr, policy, cm, sim, dp, skip_idle=True, on_step=on_step)
+    eng = RealtimeEngine(tr, policy, cm, sim, dp, skip_idle=True, on_step=on_step, lockstep=lockstep)
     if world > 1:
         import torch.distributed as dist
 
@@ -221,10 +240,11 @@ def run_ours(args):
     wall = state["wall1"] - state["wall0"]
     dev_s = _max_over_ranks(dev_s, world, dev)
     wall = _max_over_ranks(wall, world, dev)
-    eff = _sum_over_ranks(eff, world, dev)
-    toks = _sum_over_ranks(toks, world, dev)
-    # swap traffic of the window (bytes per token = all layers' K and V)
-    bpt = shape.kv_bytes_per_token
+    if not tp_mode:  # replicas: every rank generated its own tokens
+        eff = _sum_over_ranks(eff, world, dev)
+        toks = _sum_over_ranks(toks, world, dev)
+    # swap traffic of the window (bytes per token = all layers' K and V of this rank's shard)
+    bpt = shape.kv_bytes_per_token // tp_size
     xfers = dp.transfer_log()[state["ev0"]:state["ev1"]]
     d2h_tok = sum(n for k, n, _ in xfers if k == "d2h")
     h2d_tok = sum(n for k, n, _ in xfers if k == "h2d")
@@ -252,11 +272,23 @@ def run_ours(args):
         avg_ms = sum(ms for _, ms in per) / len(per)
         avg_bytes = sum(b for b, _ in per) / len(per)
         ach = avg_bytes / (avg_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "paged_attn_mma_kernel<4> (v3, tensor cores) + combine", "achieved": round(ach, 1),
+        roof = {"bound": "hbm", "kernel": f"paged_attn_mma_kernel<{shape.n_q_heads // shape.n_kv_heads}> (v3, tensor "
+                          "cores) + combine", "achieved": round(ach, 1),
                 "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
                 "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live),
                 "algorithmic_bytes_per_launch": round(avg_bytes),
-                "note": "bytes = sum(ctx) x 4 KiB (K+V, 8 kv heads x 128 x bf16) + q/out + table entries per layer"}
+                "note": f"bytes = sum(ctx) x {pool.H * pool.D * 4} B (K+V, {pool.H} kv heads x {pool.D} x bf16) + "
+                        "q/out + table entries per layer"}
+    # transfer hidden under decode, at the window's own swap volume per step
+    # and at a link-saturating volume (swap time ~= decode time)
+    if live and args.graphs:
+        per_step = lambda n: math.ceil(n / 16 / len(timed))  # noqa: E731
+        hid_w = measure_hidden(model, dp, eng, live, per_step(d2h_tok), per_step(h2d_tok))
+        sat = max(1, int(0.055 * (hid_w["t_decode_ms"] if hid_w else 7.0) * 1e6 / dp.pool.block_bytes))
+        hid_s = measure_hidden(model, dp, eng, live, sat, sat)
+        swap["hidden_under_decode"] = {"window_volume": hid_w, "link_saturating": hid_s,
+                                       "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = the captured "
+                                               "forward of the live batch; swaps on copy engines, own streams"}
     ttft = [r for r in res.records if r.gen_times]
     out = {
         "metric": METRIC,
@@ -269,17 +301,22 @@ def run_ours(args):
         "decode_ms_per_step": sum(s["dur"] for s in timed) / len(timed) * 1e3,
         "prefill_device_s_in_window": round(prefill_s, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if tp_mode else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (random-init Llama3-8B weights, seeded prompt token ids, frozen C2 trace)",
-        "config": {"workload": f"C2: Llama3-8B bf16 random-init, 1xB200 per replica, 256-request {args.arrivals} "
-                               "(bodies of the first 256 arrivals of the lambda=10/s 30 s trace, seed 1), KV pool "
-                               "163,840 tokens (20 GiB) + pinned host tier, block 16, max_batch 128",
-                   "model": "llama3-8b", "global_batch": max(s["batch"] for s in timed),
+        "data": f"synthetic (random-init {shape.name} weights, seeded prompt token ids, frozen C2 trace)",
+        "config": {"workload": (f"C4: Qwen2.5-32B bf16 random-init, tensor-parallel TP={world} (NCCL all-reduce "
+                                f"after o_proj / down_proj), 256-request {args.arrivals} (C2 population), KV ledger "
+                                "163,840 tokens (40 GiB over the TP ranks) + pinned host tier per rank, block 16, "
+                                "max_batch 128") if tp_mode else
+                               (f"C2: Llama3-8B bf16 random-init, 1xB200 per replica, 256-request {args.arrivals} "
+                                "(bodies of the first 256 arrivals of the lambda=10/s 30 s trace, seed 1), KV pool "
+                                "163,840 tokens (20 GiB) + pinned host tier, block 16, max_batch 128"),
+                   "model": shape.name, "global_batch": max(s["batch"] for s in timed),
                    "mean_batch": round(statistics.mean(s["batch"] for s in timed), 1),
-                   "seq_len": None, "parallelism": f"replicas x{world}", "arrivals": args.arrivals,
-                   "l2": "working set (16 GB weights + KV) >> 126 MB L2; no flush needed",
+                   "seq_len": None, "parallelism": f"tp{world}" if tp_mode else f"replicas x{world}",
+                   "arrivals": args.arrivals,
+                   "l2": "working set (weights + KV, tens of GB) >> 126 MB L2; no flush needed",
                    "timed_region": f"decode iterations [{args.warmup}, {args.warmup + args.steps}) from t=0 "
                                    "of the real-time loop (measured clock, idle gaps skipped)",
                    "cuda_graphs": bool(args.graphs), "fused_write_through": bool(args.fused_wt)},
@@ -311,6 +348,66 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return out
+
+
+def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=24):
+    """Transfer hidden under decode: the real decode step (the
+    captured Llama3-8B forward of the live batch) S times alone, the swap
+    traffic alone (``blocks_out`` 2 MiB blocks gathered to pinned host on the
+    evict stream + ``blocks_in`` scattered from it on the load stream, per
+    step, copy engines), and both concurrently.
+    hidden = 1 - (T_both - T_decode) / T_swap.  Runs after the timed window on
+    free pool / host blocks (no live KV is touched)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2510_02758_b200 import _lib
+
+    pool = dp.pool
+    nb = max(blocks_out, blocks_in)
+    if nb == 0 or pool.free_count(_lib.TIER_GPU) < nb or pool.free_count(_lib.TIER_HOST) < 2 * nb:
+        return None
+    g = pool.alloc(_lib.TIER_GPU, nb)
+    h = pool.alloc(_lib.TIER_HOST, 2 * nb)
+    segs_out = dp._seg_array([(g[i], h[i], 0, 16) for i in range(blocks_out)])
+    segs_in = dp._seg_array([(g[i], h[nb + i], 0, 16) for i in range(blocks_in)])
+    pos = [eng.state[r].kv.total_kv - 1 for r in rids]
+    st = dp.s_compute
+
+    def decode():
+        with torch.cuda.stream(st):
+            model._decode_graph(dp, rids, pos, st)
+
+    def swaps():
+        if blocks_out:
+            _lib.check(_lib.lib.tf_kv_gather_d2h(pool.handle, segs_out, blocks_out, 0, pool.L, _lib.ENGINE_CE,
+                                                 C.c_void_p(dp.s_evict.cuda_stream)))
+        if blocks_in:
+            _lib.check(_lib.lib.tf_kv_scatter_h2d(pool.handle, segs_in, blocks_in, 0, pool.L, _lib.ENGINE_CE,
+                                                  C.c_void_p(dp.s_load.cuda_stream)))
+
+    def run(fns):
+        for f in fns:
+            f()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            for f in fns:
+                f()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / steps
+
+    t_dec = run([decode])
+    t_swp = run([swaps])
+    t_both = run([decode, swaps])
+    pool.free(_lib.TIER_GPU, g)
+    pool.free(_lib.TIER_HOST, h)
+    return {"blocks_out_per_step": blocks_out, "blocks_in_per_step": blocks_in, "batch": len(rids),
+            "t_decode_ms": round(t_dec * 1e3, 3), "t_swap_ms": round(t_swp * 1e3, 3),
+            "t_both_ms": round(t_both * 1e3, 3),
+            "swap_gbs": round((blocks_out + blocks_in) * pool.block_bytes / t_swp / 1e9, 2),
+            "hidden_frac": round(1.0 - max(0.0, t_both - t_dec) / t_swp, 4)}
 
 
 def cpu_baseline(args, timed, quick=False):
@@ -350,6 +447,8 @@ def main():
     ap.add_argument("--swap-engine", type=int, default=2, help="0 SM kernel, 1 copy engines, 2 auto (whole "
                     "blocks on copy engines, partial blocks on the SM kernel)")
     ap.add_argument("--arrivals", default="burst", choices=["burst", "poisson"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c4"], help="c2: Llama3-8B replicas (C2/C3, default); "
+                    "c4: Qwen2.5-32B tensor-parallel over the launched ranks")
     ap.add_argument("--graphs", type=int, default=1)
     ap.add_argument("--fused-wt", type=int, default=1, help="mirror KV to the host inside the prefill/decode "
                     "epilogue (SURVEY 8f #1) instead of separate write-through chunks")
@@ -366,7 +465,8 @@ def main():
         try:
             avail_kb = next(int(line.split()[1]) for line in open("/proc/meminfo") if line.startswith("MemAvailable"))
             world = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1"))))
-            cap = int(avail_kb * 1024 * 0.6 / world / (2 << 20))
+            blk = (4 << 20) // world if args.config == "c4" else (2 << 20)  # pinned bytes per host block
+            cap = int(avail_kb * 1024 * 0.6 / world / blk)
             args.host_blocks = max(1024, min(args.host_blocks, cap))
         except (OSError, StopIteration, ValueError):
             pass

@@ -8,6 +8,9 @@ C2  Llama3-8B bf16, 1xB200, 256-request Poisson burst (lambda=10, first 256
     tokens (20 GiB, 10,240 blocks) so that about 25% of the burst's peak
     footprint fits (the paper's mem-frac=0.3).
 C3  C2 request-sharded over G replicas (request i -> replica i mod G).
+C4  Qwen2.5-32B bf16, tensor-parallel over TP = 1/2/4/8 B200s (NCCL), the C2
+    request population and ledger (163,840 tokens; 256 KiB of KV per token,
+    split over the TP ranks' pools and host links).
 C5  KV swap sweep (block counts 1..64K) - see bench_swap.py.
 
 Each config can build the reference-shaped dataclasses from *any* module
@@ -32,6 +35,7 @@ class ModelShape:
     vocab: int
     rope_theta: float = 500000.0
     rms_eps: float = 1e-5
+    qkv_bias: bool = False  # Qwen2 family: bias on the q/k/v projections
 
     @property
     def kv_bytes_per_token_layer(self) -> int:
@@ -48,7 +52,8 @@ TINY = ModelShape("tiny-decoder", n_layers=2, hidden=256, n_q_heads=4, n_kv_head
 LLAMA3_8B = ModelShape("llama3-8b", n_layers=32, hidden=4096, n_q_heads=32, n_kv_heads=8,
                        head_dim=128, ffn=14336, vocab=128256)
 QWEN25_32B = ModelShape("qwen2.5-32b", n_layers=64, hidden=5120, n_q_heads=40, n_kv_heads=8,
-                        head_dim=128, ffn=27648, vocab=152064, rope_theta=1000000.0, rms_eps=1e-6)
+                        head_dim=128, ffn=27648, vocab=152064, rope_theta=1000000.0, rms_eps=1e-6,
+                        qkv_bias=True)
 
 
 @dataclass(frozen=True)
@@ -144,4 +149,20 @@ C2 = ServingConfig(
     duration=30.0,
 )
 
-CONFIGS = {"c1": C1, "c2": C2}
+
+
+def c4(tp: int = 1) -> ServingConfig:
+    """C4 at tensor-parallel degree ``tp``.  Cost-model priors per rank:
+    decode 65.5 GB / TP of weights at ~6.5 TB/s + launch overhead; 256 KiB / TP
+    of KV per context token; prefill ~64 GFLOP/token / TP at ~0.8 PFLOP/s;
+    PCIe ~55 GB/s per rank link / (256 KiB / TP) per token."""
+    from dataclasses import replace
+
+    return replace(
+        C2, name=f"c4-qwen2.5-32b-tp{tp}", model=QWEN25_32B,
+        cost=dict(prefill_per_token=8e-5 / tp, decode_base=10.5e-3 / tp, decode_per_request=4e-5 / tp,
+                  decode_per_ctx_token=4e-8 / tp, h2d_bandwidth=210000 * tp, d2h_bandwidth=210000 * tp),
+        sched=dict(C2.sched, per_request_mem_estimate=3100.0))
+
+
+CONFIGS = {"c1": C1, "c2": C2, "c4": c4(1)}

@@ -523,6 +523,13 @@ class GpuDataPlane:
         self.attn_out = (list(batch), pos, out)
 
     # ------------------------------------------------------------ inspection
+    def record_event(self):
+        """Timing event at the current tail of the compute stream (the
+        real-time engine's completion / clock-anchor events)."""
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(self.s_compute)
+        return ev
+
     def synchronize(self):
         for s in {self.s_compute, self.s_evict, self.s_load}:
             s.synchronize()

@@ -28,28 +28,50 @@ from ._lib import check, lib
 
 
 class PagedDecoder:
-    def __init__(self, shape, device="cuda", seed=0, dtype=torch.bfloat16, max_batch=256):
+    def __init__(self, shape, device="cuda", seed=0, dtype=torch.bfloat16, max_batch=256, tp=None):
+        """``tp`` (tp.TpGroup): keep this rank's 1/TP of the heads / MLP columns
+        (C4).  Each weight is drawn in full with the same generator stream as
+        TP=1 and sliced, so a TP model is the TP=1 model partitioned."""
         self.s = shape
+        self.tp = tp
         self.device = torch.device(device)
         g = torch.Generator(device=self.device).manual_seed(seed)
         d, hq, hkv, hd, ffn = shape.hidden, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, shape.ffn
+        rank, size = (tp.rank, tp.size) if tp is not None else (0, 1)
+        if hkv % size or ffn % size:
+            raise ValueError(f"TP={size} does not divide {hkv} kv heads / ffn {ffn}")
+        self.hq, self.hkv, self.ffn = hq // size, hkv // size, ffn // size
+        qc = slice(rank * self.hq * hd, (rank + 1) * self.hq * hd)
+        kc = slice(hq * hd + rank * self.hkv * hd, hq * hd + (rank + 1) * self.hkv * hd)
+        vc = slice((hq + hkv) * hd + rank * self.hkv * hd, (hq + hkv) * hd + (rank + 1) * self.hkv * hd)
+        fc = slice(rank * self.ffn, (rank + 1) * self.ffn)
 
         def w(*dims):
             t = torch.empty(*dims, device=self.device, dtype=dtype)
             t.normal_(0.0, 0.02, generator=g)
             return t
 
+        def shard_qkv(t):  # [.., (hq + 2 hkv) hd] -> [.., (hq + 2 hkv)/TP hd] as [q | k | v]
+            return t if size == 1 else torch.cat([t[..., qc], t[..., kc], t[..., vc]], -1).contiguous()
+
+        def shard_gu(t):  # [d, 2 ffn] -> [d, 2 ffn/TP] as [gate | up]
+            return t if size == 1 else torch.cat([t[:, fc], t[:, ffn:][:, fc]], -1).contiguous()
+
         self.embed = w(shape.vocab, d)
         self.layers = []
         for _ in range(shape.n_layers):
-            self.layers.append({
-                "ln1": torch.ones(d, device=self.device, dtype=dtype),
-                "wqkv": w(d, (hq + 2 * hkv) * hd),
-                "wo": w(hq * hd, d),
-                "ln2": torch.ones(d, device=self.device, dtype=dtype),
-                "wgu": w(d, 2 * ffn),
-                "wd": w(ffn, d),
-            })
+            L = {"ln1": torch.ones(d, device=self.device, dtype=dtype),
+                 "wqkv": shard_qkv(w(d, (hq + 2 * hkv) * hd))}
+            if shape.qkv_bias:
+                L["bqkv"] = shard_qkv(w((hq + 2 * hkv) * hd))
+            wo = w(hq * hd, d)
+            L["wo"] = wo if size == 1 else wo[qc].contiguous()
+            L["ln2"] = torch.ones(d, device=self.device, dtype=dtype)
+            L["wgu"] = shard_gu(w(d, 2 * ffn))
+            wd = w(ffn, d)
+            L["wd"] = wd if size == 1 else wd[fc].contiguous()
+            del wo, wd
+            self.layers.append(L)
         self.ln_f = torch.ones(d, device=self.device, dtype=dtype)
         self.lm_head = w(d, shape.vocab)
         inv = 1.0 / (shape.rope_theta ** (torch.arange(0, hd, 2, device=self.device, dtype=torch.float32) / hd))
@@ -90,11 +112,22 @@ class PagedDecoder:
                                C.c_void_p(pos.data_ptr()), n, layer, C.c_void_p(k.data_ptr()),
                                C.c_void_p(v.data_ptr()), k.stride(0), C.c_void_p(stream.cuda_stream)), "tf_kv_append")
 
+    def _proj_residual(self, x, a, w):
+        """x + a @ w; under TP each rank holds a row slice of w, rank 0 adds the
+        residual and one all-reduce (sum) completes both."""
+        if self.tp is None or self.tp.size == 1:
+            return torch.addmm(x, a, w)
+        y = torch.addmm(x, a, w) if self.tp.rank == 0 else a @ w
+        return self.tp.all_reduce(y)
+
+    def _qkv(self, h, L):
+        return torch.addmm(L["bqkv"], h, L["wqkv"]) if "bqkv" in L else h @ L["wqkv"]
+
     def _mlp(self, x, L):
         h = self._rms(x, L["ln2"])
         gu = h @ L["wgu"]
         g, u = gu.chunk(2, dim=-1)
-        return torch.addmm(x, F.silu(g) * u, L["wd"])
+        return self._proj_residual(x, F.silu(g) * u, L["wd"])
 
     # ------------------------------------------------------------ forward passes
     @torch.no_grad()
@@ -110,27 +143,27 @@ class PagedDecoder:
                             dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
         rows, pos32 = meta[:, 0].contiguous(), meta[:, 1].contiguous()
         n = toks.numel()
-        G = s.n_q_heads // s.n_kv_heads
+        G = self.hq // self.hkv
         x = self.embed[toks]
-        q = torch.empty((n, s.n_q_heads, s.head_dim), device=self.device, dtype=x.dtype)
-        kvb = torch.empty((2, n, s.n_kv_heads, s.head_dim), device=self.device, dtype=x.dtype)
+        q = torch.empty((n, self.hq, s.head_dim), device=self.device, dtype=x.dtype)
+        kvb = torch.empty((2, n, self.hkv, s.head_dim), device=self.device, dtype=x.dtype)
         k, v = kvb[0], kvb[1]
         for li, L in enumerate(self.layers):
             h = self._rms(x, L["ln1"])
-            qkv = h @ L["wqkv"]
+            qkv = self._qkv(h, L)
             # rotary q/k + paged K/V append (+ host mirror when write-through is
             # fused) + contiguous k/v for the prompt attention
             if getattr(dp, "fused_wt", False):
                 check(lib.tf_rope_kv_append_wt(dp.pool.handle, C.c_void_p(dp.table.data_ptr()),
                                                C.c_void_p(dp.htable.data_ptr()), dp.nlb, C.c_void_p(rows.data_ptr()),
                                                C.c_void_p(pos32.data_ptr()), n, li, C.c_void_p(qkv.data_ptr()),
-                                               s.n_q_heads, C.c_void_p(self._inv_freq.data_ptr()),
+                                               self.hq, C.c_void_p(self._inv_freq.data_ptr()),
                                                C.c_void_p(q.data_ptr()), C.c_void_p(kvb.data_ptr()),
                                                C.c_void_p(st.cuda_stream)), "tf_rope_kv_append_wt")
             else:
                 check(lib.tf_rope_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb,
                                             C.c_void_p(rows.data_ptr()), C.c_void_p(pos32.data_ptr()), n, li,
-                                            C.c_void_p(qkv.data_ptr()), s.n_q_heads,
+                                            C.c_void_p(qkv.data_ptr()), self.hq,
                                             C.c_void_p(self._inv_freq.data_ptr()), C.c_void_p(q.data_ptr()),
                                             C.c_void_p(kvb.data_ptr()), C.c_void_p(st.cuda_stream)),
                       "tf_rope_kv_append")
@@ -143,7 +176,7 @@ class PagedDecoder:
                     outs.append(F.scaled_dot_product_attention(qi, ki, vi, is_causal=True)[0].transpose(0, 1))
                     o += ln
             a = torch.cat(outs).reshape(n, -1)
-            x = torch.addmm(x, a, L["wo"])
+            x = self._proj_residual(x, a, L["wo"])
             x = self._mlp(x, L)
         last = torch.tensor(list(_cumsum(lens)), device=self.device) - 1
         return (self._rms(x[last], self.ln_f) @ self.lm_head).argmax(-1)
@@ -218,12 +251,12 @@ class PagedDecoder:
         with torch.cuda.stream(st):
             rows = torch.tensor(rids, dtype=torch.int32, device=self.device)
             ctx = torch.tensor([p + 1 for p in positions], dtype=torch.int32, device=self.device)
-            q = torch.randn((B, s.n_q_heads, s.head_dim), device=self.device).to(torch.bfloat16)
+            q = torch.randn((B, self.hq, s.head_dim), device=self.device).to(torch.bfloat16)
             out = torch.empty_like(q)
             max_ctx = max(positions) + 1
-            ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, s.n_q_heads)))
+            ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, self.hq)))
             ws = torch.empty(ws_n, dtype=torch.uint8, device=self.device)
-            abytes = (sum(positions) + B) * 2 * s.n_kv_heads * s.head_dim * 2 + 2 * B * s.n_q_heads * s.head_dim * 2 \
+            abytes = (sum(positions) + B) * 2 * self.hkv * s.head_dim * 2 + 2 * B * self.hq * s.head_dim * 2 \
                 + sum((p + 16) // 16 for p in positions) * 4
             res = []
             for r in range(reps + 1):
@@ -233,7 +266,7 @@ class PagedDecoder:
                     check(lib.tf_paged_decode_attn(dp.pool.handle, C.c_void_p(q.data_ptr()),
                                                    C.c_void_p(dp.table.data_ptr()), dp.nlb,
                                                    C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B,
-                                                   max_ctx, li, s.n_q_heads, self.scale, C.c_void_p(out.data_ptr()),
+                                                   max_ctx, li, self.hq, self.scale, C.c_void_p(out.data_ptr()),
                                                    C.c_void_p(ws.data_ptr()), ws_n, C.c_void_p(st.cuda_stream)),
                           "tf_paged_decode_attn")
                     e1.record(st)
@@ -262,7 +295,7 @@ class PagedDecoder:
             io = torch.zeros((3, Bp), dtype=torch.int64, device=self.device)
             io[1].fill_(dp.scratch_row)
             stage = torch.zeros((3, Bp), dtype=torch.int64, pin_memory=True)
-            ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, Bp, self._gmax_ctx, s.n_q_heads)))
+            ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, Bp, self._gmax_ctx, self.hq)))
             ws = torch.empty(ws_n, dtype=torch.uint8, device=self.device)
             with torch.cuda.stream(st):
                 self._forward_graphable(dp, io, Bp, ws, st)  # warm-up (kernel attributes, cuBLAS handles)
@@ -302,7 +335,7 @@ class PagedDecoder:
         pos32 = torch.tensor(positions, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
         ctx = pos32 + 1
         max_ctx = max(positions) + 1
-        need = int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, s.n_q_heads))
+        need = int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, self.hq))
         if need > self._ws.numel():
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         return self._layers_decode(dp, tokens, rows, pos32, ctx, B, max_ctx, self._ws, st, self.attn_timing,
@@ -311,29 +344,29 @@ class PagedDecoder:
     def _layers_decode(self, dp, tokens, rows, pos32, ctx, B, max_ctx, ws, st, timing, positions=None):
         s = self.s
         x = self.embed[tokens]
-        attn = torch.empty((B, s.n_q_heads, s.head_dim), device=self.device, dtype=x.dtype)
+        attn = torch.empty((B, self.hq, s.head_dim), device=self.device, dtype=x.dtype)
         if timing is not None:
             # algorithmic bytes of one launch: K+V of every context token, q in,
             # out, block-table entries
-            abytes = (sum(positions) + B) * 2 * s.n_kv_heads * s.head_dim * 2 + 2 * B * s.n_q_heads * s.head_dim * 2 \
+            abytes = (sum(positions) + B) * 2 * self.hkv * s.head_dim * 2 + 2 * B * self.hq * s.head_dim * 2 \
                 + sum((p + 16) // 16 for p in positions) * 4
-        q = torch.empty((B, s.n_q_heads, s.head_dim), device=self.device, dtype=x.dtype)
+        q = torch.empty((B, self.hq, s.head_dim), device=self.device, dtype=x.dtype)
         for li, L in enumerate(self.layers):
             h = self._rms(x, L["ln1"])
-            qkv = h @ L["wqkv"]
+            qkv = self._qkv(h, L)
             # fused rotary embedding + paged K/V append + q layout (one launch)
             if getattr(dp, "fused_wt", False):
                 # write-through fused into the append epilogue (host mirror in the same step)
                 check(lib.tf_rope_kv_append_wt(dp.pool.handle, C.c_void_p(dp.table.data_ptr()),
                                                C.c_void_p(dp.htable.data_ptr()), dp.nlb, C.c_void_p(rows.data_ptr()),
                                                C.c_void_p(pos32.data_ptr()), B, li, C.c_void_p(qkv.data_ptr()),
-                                               s.n_q_heads, C.c_void_p(self._inv_freq.data_ptr()),
+                                               self.hq, C.c_void_p(self._inv_freq.data_ptr()),
                                                C.c_void_p(q.data_ptr()), None, C.c_void_p(st.cuda_stream)),
                       "tf_rope_kv_append_wt")
             else:
                 check(lib.tf_rope_kv_append(dp.pool.handle, C.c_void_p(dp.table.data_ptr()), dp.nlb,
                                             C.c_void_p(rows.data_ptr()), C.c_void_p(pos32.data_ptr()), B, li,
-                                            C.c_void_p(qkv.data_ptr()), s.n_q_heads,
+                                            C.c_void_p(qkv.data_ptr()), self.hq,
                                             C.c_void_p(self._inv_freq.data_ptr()), C.c_void_p(q.data_ptr()), None,
                                             C.c_void_p(st.cuda_stream)), "tf_rope_kv_append")
             if timing is not None:
@@ -341,13 +374,13 @@ class PagedDecoder:
                 e0.record(st)
             check(lib.tf_paged_decode_attn(dp.pool.handle, C.c_void_p(q.data_ptr()), C.c_void_p(dp.table.data_ptr()),
                                            dp.nlb, C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B, max_ctx,
-                                           li, s.n_q_heads, self.scale, C.c_void_p(attn.data_ptr()),
+                                           li, self.hq, self.scale, C.c_void_p(attn.data_ptr()),
                                            C.c_void_p(ws.data_ptr()), ws.numel(),
                                            C.c_void_p(st.cuda_stream)), "tf_paged_decode_attn")
             if timing is not None:
                 e1.record(st)
                 timing.append((abytes, e0, e1))
-            x = torch.addmm(x, attn.view(B, -1), L["wo"])
+            x = self._proj_residual(x, attn.view(B, -1), L["wo"])
             x = self._mlp(x, L)
         return (self._rms(x, self.ln_f) @ self.lm_head).argmax(-1)
 

@@ -13,6 +13,14 @@ wall clock and every duration comes from the hardware:
   ``update_rate_ema`` exactly like the reference's simulated ones;
 * readers consume on the same clock at their configured rates.
 
+``lockstep`` (tensor parallelism, C4): every TP rank runs this same engine
+on its own shard; completions are agreed with one small collective per
+loop iteration (``Lockstep.agree``: a completion counts once it fired on
+EVERY rank, at the LATEST rank's time; the clock is the latest rank's), so
+all ranks see the same event sequence at the same times and the
+deterministic engine + bit-exact selector take identical decisions with no
+decision broadcast.
+
 ``skip_idle``: when the GPU and both copy streams are idle and the next
 event is a reader / arrival / tick in the future, the clock jumps to it
 instead of sleeping (nothing is in flight, so no measured duration spans a
@@ -24,8 +32,6 @@ from __future__ import annotations
 
 import heapq
 import time
-
-import torch
 
 from .engine import (
     CHUNK_TRANSFER_DONE,
@@ -40,8 +46,10 @@ from .engine import (
 
 
 class RealtimeEngine(Engine):
-    def __init__(self, trace, policy, cm, sim, dataplane, skip_idle: bool = True, on_step=None, max_steps=None):
+    def __init__(self, trace, policy, cm, sim, dataplane, skip_idle: bool = True, on_step=None, max_steps=None,
+                 lockstep=None):
         super().__init__(trace, policy, cm, sim, dataplane)
+        self.lockstep = lockstep
         assert dataplane is not None and dataplane.mode == "realtime"
         self.skip_idle = skip_idle
         self.on_step = on_step  # callback(record dict) after every decode iteration
@@ -73,8 +81,7 @@ class RealtimeEngine(Engine):
         return time.perf_counter() - self._t0 + self.skipped_s
 
     def _reanchor(self):
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record(self.dp.s_compute)
+        ev = self.dp.record_event()
         ev.synchronize()
         self._anchor = (ev, self._clock())
 
@@ -117,9 +124,7 @@ class RealtimeEngine(Engine):
         self._gpu = ("decode", batch, start, self._end_event())
 
     def _end_event(self):
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record(self.dp.s_compute)
-        return ev
+        return self.dp.record_event()
 
     def _start_channel(self, time_, ch_):
         if ch_.in_service is not None or not ch_.queue:
@@ -138,15 +143,21 @@ class RealtimeEngine(Engine):
         self._lanes[ch_.direction] = (time_, ev)
 
     # ------------------------------------------------------------------- loop
-    def _poll_completions(self) -> bool:
-        done = []
-        if self._gpu is not None and self._gpu[3].query():
-            done.append((self._event_time(self._gpu[3]), 0, "gpu"))
-        for d, v in self._lanes.items():
-            if v is not None and v[1].query():
-                done.append((max(self._event_time(v[1]), v[0]), 1, d))
+    def _poll_completions(self):
+        """-> (progressed, clock).  Lockstep: completions and clock agreed over ranks."""
+        slots = (("gpu", self._gpu, 3, 0), ("d2h", self._lanes["d2h"], 1, 1), ("h2d", self._lanes["h2d"], 1, 1))
+        flags, times = [], []
+        for what, v, i, _ in slots:
+            ok = v is not None and v[i].query()
+            flags.append(ok)
+            t = self._event_time(v[i]) if ok else 0.0
+            times.append(max(t, v[0]) if ok and what != "gpu" else t)
+        clock = self._clock()
+        if self.lockstep is not None:
+            clock, flags, times = self.lockstep.agree(clock, flags, times)
+        done = [(t, order, what) for (what, _, _, order), ok, t in zip(slots, flags, times) if ok]
         if not done:
-            return False
+            return False, clock
         done.sort()
         for t, _, what in done:
             self.now = max(self.now, t)
@@ -165,7 +176,7 @@ class RealtimeEngine(Engine):
             else:
                 self._lanes[what] = None
                 self._on_chunk_transfer_done(t, -1, what)
-        return True
+        return True, clock
 
     def _record_step(self, batch, start, end, dur):
         self._step_pre = {r: (self.state[r].status, self.state[r].generated) for r in batch}
@@ -198,8 +209,7 @@ class RealtimeEngine(Engine):
         wall0 = time.perf_counter()
         idle_spins = 0
         while self.live > 0 and not self._stop:
-            progressed = self._poll_completions()
-            now = self._clock()
+            progressed, now = self._poll_completions()
             while self._heap and self._heap[0][0] <= now:
                 t, _, subject, seq = heapq.heappop(self._heap)
                 kind, payload = self._payload.pop(seq)
@@ -216,7 +226,7 @@ class RealtimeEngine(Engine):
             if not busy:
                 if not self._heap:
                     raise DeadlockError(f"{self.live} requests incomplete but nothing is scheduled")
-                gap = self._heap[0][0] - self._clock()
+                gap = self._heap[0][0] - now
                 if gap > 0:
                     if self.skip_idle:
                         self.skipped_s += gap

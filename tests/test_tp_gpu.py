@@ -1,0 +1,101 @@
+"""C4 tensor-parallel sharding on ONE GPU: the TP=2 model (two shards driven by
+two threads, their all-reduce done through shared memory on the same device)
+writes the same paged KV and computes the same tokens as the TP=1 model -
+i.e. a TP model is the TP=1 model partitioned (model.PagedDecoder(tp=...)).
+The NCCL transport itself is torch.distributed's; only the partitioning and
+the residual-on-rank-0 all-reduce placement are under test."""
+import threading
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+class ThreadTp:
+    """TpGroup stand-in: ranks are threads on one device; all_reduce sums the
+    ranks' tensors in rank order (every rank computes the same sum)."""
+
+    def __init__(self, rank, size, shared):
+        self.rank, self.size, self.sh = rank, size, shared
+
+    def all_reduce(self, x):
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        self.sh["buf"][self.rank] = x
+        self.sh["bar"].wait()
+        acc = self.sh["buf"][0].float()
+        for r in range(1, self.size):
+            acc = acc + self.sh["buf"][r].float()
+        torch.cuda.current_stream().synchronize()
+        self.sh["bar"].wait()
+        x.copy_(acc.to(x.dtype))
+        torch.cuda.current_stream().synchronize()
+        return x
+
+
+def _setup(cuda, shape, tp, n_req, nlb):
+    import torch
+
+    from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
+    from paper_2510_02758_b200.model import PagedDecoder
+    from paper_2510_02758_b200.workload import RequestSpec
+
+    size = tp.size if tp else 1
+    reqs = [RequestSpec(i, 0.0, 40 + 7 * i, 50, 20.0) for i in range(n_req)]
+    pool = KvPool(n_req * nlb + 2, 1, shape.n_layers, shape.n_kv_heads // size, shape.head_dim, device=cuda)
+    pool.gpu.zero_()
+    model = PagedDecoder(shape, device=cuda, seed=3, tp=tp)
+    dp = GpuDataPlane(reqs, pool, mode="realtime", kv_source="model", model=model,
+                      n_q_heads=shape.n_q_heads // size)
+    dp.table[:n_req, :nlb] = torch.arange(n_req * nlb, dtype=torch.int32, device=cuda).view(n_req, nlb)
+    return model, dp, pool
+
+
+@pytest.mark.parametrize("qkv_bias", [False, True])
+def test_tp2_equals_tp1(cuda, qkv_bias):
+    import dataclasses
+
+    import torch
+
+    from paper_2510_02758_b200 import configs
+
+    shape = dataclasses.replace(configs.TINY, qkv_bias=qkv_bias)
+    n_req, nlb = 4, 5
+    seqs = [(i, torch.randint(0, shape.vocab, (30 + 9 * i,), generator=torch.Generator().manual_seed(i)), 0)
+            for i in range(n_req)]
+    m1, dp1, pool1 = _setup(cuda, shape, None, n_req, nlb)
+    with torch.cuda.stream(dp1.s_compute):
+        tok1 = m1._prefill_batch(dp1, seqs, dp1.s_compute)
+    torch.cuda.synchronize()
+
+    shared = {"buf": [None, None], "bar": threading.Barrier(2)}
+    outs = [None, None]
+    shards = [_setup(cuda, shape, ThreadTp(r, 2, shared), n_req, nlb) for r in range(2)]
+
+    def run(r):
+        m, dp, _ = shards[r]
+        with torch.cuda.stream(dp.s_compute):
+            outs[r] = m._prefill_batch(dp, seqs, dp.s_compute)
+        dp.s_compute.synchronize()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]), "TP ranks disagree on the sampled tokens"
+    # sampled tokens: argmax over a 4096 vocabulary; allow a rare near-tie flip
+    assert (outs[0] == tok1).float().mean().item() >= 0.75
+    # KV: shard r's pool holds kv head r of the TP=1 pool, layer by layer
+    v1 = pool1.gpu_view().view(torch.bfloat16).float()
+    for r in range(2):
+        vr = shards[r][2].gpu_view().view(torch.bfloat16).float()
+        ref = v1[:, :, :, r:r + 1]
+        used = n_req * nlb
+        err = (vr[:used] - ref[:used]).abs().max().item()
+        assert err <= 2e-2 * max(1.0, ref[:used].abs().max().item()), f"rank {r} KV differs by {err}"
+        # layer 0 K/V do not depend on any all-reduce: equal up to GEMM blocking
+        e0 = (vr[:used, 0] - ref[:used, 0]).abs().max().item()
+        assert e0 <= 1e-2 * max(1.0, ref[:used, 0].abs().max().item())
