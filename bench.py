@@ -217,6 +217,8 @@ def run_ours(args):
                     eng._stop = True
 
     eng = RealtimeEngine(tr, policy, cm, sim, dp, skip_idle=True, on_step=on_step, lockstep=lockstep)
+    if args.watchdog:
+        _start_watchdog(eng, dp, args.watchdog)
     if world > 1:
         import torch.distributed as dist
 
@@ -272,8 +274,11 @@ def run_ours(args):
         avg_ms = sum(ms for _, ms in per) / len(per)
         avg_bytes = sum(b for b, _ in per) / len(per)
         ach = avg_bytes / (avg_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": f"paged_attn_mma_kernel<{shape.n_q_heads // shape.n_kv_heads}> (v3, tensor "
-                          "cores) + combine", "achieved": round(ach, 1),
+        G = shape.n_q_heads // shape.n_kv_heads
+        kname = {"1": "paged_attn_kernel (v1)", "2": "paged_attn_tma_kernel (v2)",
+                 "3": f"paged_attn_mma_kernel<{G}> (v3) + combine"}.get(
+            os.environ.get("TF_ATTN_IMPL", "4")[:1], f"paged_attn_stream_kernel<{G}> (v4 stream-K, tensor cores)")
+        roof = {"bound": "hbm", "kernel": kname, "achieved": round(ach, 1),
                 "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
                 "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live),
                 "algorithmic_bytes_per_launch": round(avg_bytes),
@@ -284,7 +289,8 @@ def run_ours(args):
     if live and args.graphs:
         per_step = lambda n: math.ceil(n / 16 / len(timed))  # noqa: E731
         hid_w = measure_hidden(model, dp, eng, live, per_step(d2h_tok), per_step(h2d_tok))
-        sat = max(1, int(0.055 * (hid_w["t_decode_ms"] if hid_w else 7.0) * 1e6 / dp.pool.block_bytes))
+        # blocks per direction that keep a ~55 GB/s link busy for one decode step
+        sat = max(1, int(55e9 * (hid_w["t_decode_ms"] if hid_w else 7.0) / 1e3 / dp.pool.block_bytes))
         hid_s = measure_hidden(model, dp, eng, live, sat, sat)
         swap["hidden_under_decode"] = {"window_volume": hid_w, "link_saturating": hid_s,
                                        "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = the captured "
@@ -348,6 +354,32 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return out
+
+
+def _start_watchdog(eng, dp, period):
+    """Debug aid: dump the engine's state (and every thread's stack) every
+    ``period`` seconds to stderr."""
+    import collections
+    import faulthandler
+
+    def loop():
+        while True:
+            time.sleep(period)
+            st = collections.Counter(s.status for s in eng.state.values())
+            print(f"[watchdog] now={eng.now:.3f} steps={len(eng.steps)} live={eng.live} status={dict(st)} "
+                  f"gpu={eng._gpu[0] if eng._gpu else None} lanes={[k for k, v in eng._lanes.items() if v]} "
+                  f"d2hq={len(eng.d2h.queue)} h2dq={len(eng.h2d.queue)} h2d_head="
+                  f"{eng.h2d.queue[0].tokens if eng.h2d.queue else None} mem_used={eng.mem_used} "
+                  f"committed={eng.mem_committed} free={eng._mem_free()} heap={len(eng._heap)} "
+                  f"heap0={eng._heap[0][:2] if eng._heap else None} skipped={eng.skipped_s:.2f} "
+                  f"pre={eng.total_preemptions} prefillq={len(eng.prefill_queue)} "
+                  f"gpu_free_blocks={dp.pool.free_count(0)} host_free={dp.pool.free_count(1)} "
+                  f"rates d2h={eng.measured_d2h:.0f} h2d={eng.measured_h2d:.0f} tok/s "
+                  f"prefill={eng._prefill_s_per_token():.3e} s/tok rc={eng.total_recomputes}",
+                  file=sys.stderr, flush=True)
+            faulthandler.dump_traceback(file=sys.stderr, all_threads=True)
+
+    threading.Thread(target=loop, daemon=True).start()
 
 
 def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=24):
@@ -457,6 +489,7 @@ def main():
     ap.add_argument("--ref-batch", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--watchdog", type=float, default=0.0, help="debug: dump engine state every N seconds")
     args = ap.parse_args()
     if args.host_blocks <= 0:
         args.host_blocks = 26000 if args.full_run else 16384

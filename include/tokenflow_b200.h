@@ -95,6 +95,12 @@ int tf_kv_gather_d2h(int64_t pool, const tf_seg* segs, int32_t n_segs, int32_t l
 int tf_kv_scatter_h2d(int64_t pool, const tf_seg* segs, int32_t n_segs, int32_t layer_begin, int32_t layer_end,
                       int32_t engine, void* stream);
 
+/* Zero-copy small copy through one CTA (either side may be pinned host memory,
+ * which is device-addressable under UVA): the per-step token ids / positions
+ * in and sampled ids out, so a decode step never waits behind bulk KV
+ * transfers queued on the copy engines.  bytes <= 64 MiB. */
+int tf_copy_small(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* ---------------------------------------------------------------- KV append --
  * Model path: write K/V rows of n tokens for one layer, token i at
  * (table[rows[i]], pos[i]).  k/v: [n][kv_heads][head_dim] bf16 with a row
@@ -143,7 +149,15 @@ int tf_q_fill_synthetic(void* q, const int32_t* dev_rids, const int32_t* dev_pos
  * out[b][h] = softmax(q[b][h] . K[0:ctx[b]]^T * scale) V[0:ctx[b]] over the
  * paged KV of layer `layer` of request row rows[b]; GQA head h reads kv head
  * h / (n_q_heads/kv_heads).  q/out: [B][n_q_heads][head_dim] bf16.
- * fp32 accumulation, split-KV with an in-kernel combine. */
+ * fp32 accumulation on tensor cores (mma.sync bf16).  Default (v4, head_dim
+ * 128, group <= 8, B <= 1024): stream-K - the layer's (request, kv head,
+ * block) work is split evenly over the warps of a persistent grid; segments
+ * shared by several warps are merged in-kernel by the last warp to finish.
+ * max_ctx must bound every ctx[b].  The workspace (size from
+ * tf_paged_decode_attn_workspace for the same B / max_ctx / n_q_heads) must be
+ * ZERO-filled before its first use; every launch leaves its counters zero, so
+ * it can be reused (and captured in CUDA graphs) without re-zeroing.
+ * Replaces the affine decode cost of tokensim/costs.py:45-59. */
 int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, int32_t row_stride,
                          const int32_t* dev_rows, const int32_t* dev_ctx, int32_t B, int32_t max_ctx,
                          int32_t layer, int32_t n_q_heads, float scale, void* out, void* workspace,

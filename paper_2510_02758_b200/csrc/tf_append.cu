@@ -125,11 +125,32 @@ __global__ void q_synth_kernel(uint16_t* q, const int32_t* __restrict__ rids, co
   q[e] = kv_bits((uint32_t)rids[b] + 0x5000u, (uint32_t)pos[b], (uint32_t)layer, 2u, (uint32_t)h, (uint32_t)d, seed);
 }
 
+// Zero-copy small transfer (step inputs / sampled ids): one CTA moves the
+// bytes through the SMs over mapped pinned memory, so a decode step never
+// queues behind bulk KV copies on the copy engines.
+__global__ void copy_small_kernel(unsigned char* __restrict__ dst, const unsigned char* __restrict__ src,
+                                  int64_t bytes) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  const int64_t nv = vec ? bytes / 16 : 0;
+  for (int64_t i = threadIdx.x; i < nv; i += blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (int64_t i = nv * 16 + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+
 }  // namespace tf
 
 using namespace tf;
 
 extern "C" {
+
+int tf_copy_small(void* dst, const void* src, int64_t bytes, void* stream) {
+  TF_CHECK_ARG(bytes >= 0 && bytes <= (64 << 20), "tf_copy_small: bytes %lld out of range", (long long)bytes);
+  if (bytes == 0) return TF_OK;
+  TF_CHECK_ARG(dst && src, "tf_copy_small: NULL pointer");
+  copy_small_kernel<<<1, 256, 0, (cudaStream_t)stream>>>((unsigned char*)dst, (const unsigned char*)src, bytes);
+  TF_LAUNCH_CHECK();
+  return TF_OK;
+}
 
 int tf_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride, const int32_t* dev_rows,
                  const int32_t* dev_pos, int32_t n, int32_t layer, const void* k, const void* v, int64_t kv_row_stride,

@@ -49,6 +49,9 @@ struct AttnArgs {
   int64_t block_elems;
   int32_t stride, n_layers, kv_heads, layer, hq, splits, blocks_per_split;
   float scale_log2;
+  // v4 (stream-K): batch, partial slots per (request, kv head), self-resetting counters
+  int32_t B, kmax;
+  int32_t* counters;
 };
 
 // D = head_dim, G = q heads per kv head.
@@ -784,11 +787,289 @@ __global__ void __launch_bounds__(kV3Warps * 32, 2) paged_attn_mma_kernel(const 
   }
 }
 
+
+// ------------------------------------------------------------------------
+// v4: stream-K warps.  The (request, kv head, block) work of one layer is
+// flattened (request-major, then kv head, then block) and split into equal
+// contiguous ranges, one per warp of a persistent grid (2 CTAs x 4 warps per
+// SM).  Each warp streams its range through its own 3-stage cp.async ring
+// (v3's tensor-core inner loop: S = Q K^T and O += P V on mma.sync, fp32
+// online softmax) WITHOUT draining at (request, head) boundaries: the issue
+// cursor runs two blocks ahead across segment boundaries, so per-request
+// prologue / epilogue bubbles (v3's cost at short or ragged contexts) vanish
+// and every warp moves the same number of bytes.  A segment wholly inside one
+// warp writes the output directly; a segment shared by k warps writes k
+// partials and the last warp to finish (self-resetting atomic counter) merges
+// them - no second launch.
+constexpr int kV4Warps = 4;
+constexpr int kV4Stages = 3;
+constexpr int kPerMin = 8;      // minimum blocks per warp (bounds partials per segment)
+constexpr int kV4MaxB = 1024;   // requests per launch (prefix sums in shared memory)
+constexpr int kV4CtasPerSm = 2;
+
+struct SegCursor {
+  int b, kvh, j, nb;
+};
+
+__device__ __forceinline__ void seg_locate(const int* pre, int B, int kv, int f, SegCursor& c) {
+  int lo = 0, hi = B;  // largest b with pre[b] * kv <= f
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pre[mid] * kv <= f) lo = mid; else hi = mid;
+  }
+  while (lo < B - 1 && pre[lo + 1] == pre[lo]) ++lo;  // skip empty requests
+  c.b = lo;
+  c.nb = pre[lo + 1] - pre[lo];
+  const int rem = f - pre[lo] * kv;
+  c.kvh = c.nb ? rem / c.nb : 0;
+  c.j = c.nb ? rem % c.nb : 0;
+}
+
+__device__ __forceinline__ void seg_advance(const int* pre, int B, int kv, SegCursor& c) {
+  if (++c.j < c.nb) return;
+  c.j = 0;
+  if (++c.kvh < kv) return;
+  c.kvh = 0;
+  do {
+    ++c.b;
+    c.nb = c.b < B ? pre[c.b + 1] - pre[c.b] : 1;
+  } while (c.nb == 0);
+}
+
+template <int G>
+__global__ void __launch_bounds__(kV4Warps * 32, kV4CtasPerSm) paged_attn_stream_kernel(const AttnArgs a) {
+  constexpr int D = 128;
+  static_assert(G >= 1 && G <= 8, "v4 packs the group into rows 0..7 of the 16-row tile");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ int pre[kV4MaxB + 1];
+  constexpr int kTileElems = kBlk * kRowPad;
+  constexpr int kWarpElems = kV4Stages * 2 * kTileElems;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw) + warp * kWarpElems;
+  const int B = a.B, kv = a.kv_heads;
+
+  // blocks per request -> prefix sums (every CTA, ~B/32 warp scans)
+  if (warp == 0) {
+    int carry = 0;
+    if (lane == 0) pre[0] = 0;
+    for (int base = 0; base < B; base += 32) {
+      const int b = base + lane;
+      int v = b < B ? (a.ctx[b] + kBlk - 1) / kBlk : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      if (b < B) pre[b + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  const int T = pre[B] * kv;
+  const int W = gridDim.x * kV4Warps;
+  const int per = max(kPerMin, (T + W - 1) / W);
+  const int gw = blockIdx.x * kV4Warps + warp;
+  const int lo = gw * per;
+  if (lo >= T) return;
+  const int hi = min(T, lo + per);
+  const int n = hi - lo;
+
+  const int64_t tile = (int64_t)kBlk * D;
+  SegCursor ic;  // issue cursor (runs two blocks ahead of the compute cursor)
+  seg_locate(pre, B, kv, lo, ic);
+  auto issue = [&](int i) {
+    if (i < n) {
+      const int64_t koff = (((int64_t)a.layer * 2 + 0) * kv + ic.kvh) * tile;
+      const int64_t voff = (((int64_t)a.layer * 2 + 1) * kv + ic.kvh) * tile;
+      const int64_t base = (int64_t)__ldg(a.table + (int64_t)a.rows[ic.b] * a.stride + ic.j) * a.block_elems;
+      uint16_t* ks = ring + (i % kV4Stages) * 2 * kTileElems;
+      uint16_t* vs = ks + kTileElems;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ch = u * 32 + lane;
+        const int r = ch >> 4, c16 = ch & 15;
+        cp_async16(ks + r * kRowPad + c16 * 8, a.pool + base + koff + ch * 8);
+        cp_async16(vs + r * kRowPad + c16 * 8, a.pool + base + voff + ch * 8);
+      }
+      seg_advance(pre, B, kv, ic);
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+
+  const int r0 = lane >> 2, cq = (lane & 3) * 2;
+  const int lr = lane & 7, lm = lane >> 3;
+  SegCursor cc, seg;  // compute cursor; the segment being accumulated
+  seg_locate(pre, B, kv, lo, cc);
+  uint32_t qa[8][4];
+  float o[16][4];
+  float m0 = -FLT_MAX, l0 = 0.f;
+  int ctx = 0;
+
+  auto begin_segment = [&]() {
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t qlo = 0, qhi = 0;
+      if (r0 < G) {
+        const uint16_t* qrow = a.q + ((int64_t)cc.b * a.hq + cc.kvh * G + r0) * D + kk * 16 + cq;
+        qlo = *reinterpret_cast<const uint32_t*>(qrow);
+        qhi = *reinterpret_cast<const uint32_t*>(qrow + 8);
+      }
+      qa[kk][0] = qlo;
+      qa[kk][1] = 0;
+      qa[kk][2] = qhi;
+      qa[kk][3] = 0;
+    }
+#pragma unroll
+    for (int nn = 0; nn < 16; ++nn) o[nn][0] = o[nn][1] = o[nn][2] = o[nn][3] = 0.f;
+    m0 = -FLT_MAX;
+    l0 = 0.f;
+    ctx = a.ctx[cc.b];
+    seg = cc;
+  };
+
+  auto end_segment = [&](const SegCursor& sc) {
+    float l = l0;
+    l += __shfl_xor_sync(0xffffffffu, l, 1);
+    l += __shfl_xor_sync(0xffffffffu, l, 2);
+    const int S = pre[sc.b] * kv + sc.kvh * sc.nb;
+    const int first = S / per, last = (S + sc.nb - 1) / per;
+    const int64_t row0 = (int64_t)sc.b * a.hq + sc.kvh * G;
+    if (first == last) {  // the whole segment is this warp's: normalise and store
+      if (r0 < G) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        uint32_t* orow = reinterpret_cast<uint32_t*>(a.out + (row0 + r0) * D);
+#pragma unroll
+        for (int nn = 0; nn < 16; ++nn) orow[(nn * 8 + cq) >> 1] = pack_bf16(o[nn][0] * inv, o[nn][1] * inv);
+      }
+      return;
+    }
+    const int seg = sc.b * kv + sc.kvh;
+    const int64_t slot0 = (int64_t)seg * a.kmax;
+    const int64_t slot = slot0 + (gw - first);
+    if (r0 < G) {
+      float* acc = a.ws_acc + (slot * G + r0) * D;
+#pragma unroll
+      for (int nn = 0; nn < 16; ++nn)
+        *reinterpret_cast<float2*>(acc + nn * 8 + cq) = make_float2(o[nn][0], o[nn][1]);
+      if ((lane & 3) == 0) {
+        a.ws_ml[(slot * G + r0) * 2 + 0] = m0;
+        a.ws_ml[(slot * G + r0) * 2 + 1] = l;
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    int old = 0;
+    if (lane == 0) old = atomicAdd(a.counters + seg, 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    const int cnt = last - first + 1;
+    if (old != cnt - 1) return;
+    // last of the segment's warps: merge the cnt partials
+    __threadfence();
+    for (int e = lane; e < G * D; e += 32) {
+      const int g = e / D, d = e % D;
+      float mm = -FLT_MAX;
+      for (int k = 0; k < cnt; ++k) mm = fmaxf(mm, __ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2));
+      float ll = 0.f, aa = 0.f;
+      for (int k = 0; k < cnt; ++k) {
+        const float f = exp2f(__ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2) - mm);
+        ll += __ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2 + 1) * f;
+        aa += __ldcg(a.ws_acc + ((slot0 + k) * G + g) * D + d) * f;
+      }
+      a.out[(row0 + g) * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(ll > 0.f ? aa / ll : 0.f));
+    }
+    if (lane == 0) a.counters[seg] = 0;  // ready for the next launch
+  };
+
+  begin_segment();
+  for (int i = 0; i < n; ++i) {
+    if (i > 0 && cc.j == 0) {  // crossed into the next (request, kv head)
+      end_segment(seg);
+      begin_segment();
+    }
+    issue(i + 2);
+    cp_async_wait<2>();
+    __syncwarp();
+    const uint16_t* ks = ring + (i % kV4Stages) * 2 * kTileElems;
+    const uint16_t* vs = ks + kTileElems;
+    const int blk = cc.j;
+    float sfr[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t b00, b01, b10, b11;
+      const uint16_t* p = ks + ((lm >> 1) * 8 + lr) * kRowPad + kk * 16 + (lm & 1) * 8;
+      ldsm_x4(b00, b01, b10, b11, p);
+      mma_bf16(sfr[0], qa[kk], b00, b01);
+      mma_bf16(sfr[1], qa[kk], b10, b11);
+    }
+    float mx = -FLT_MAX;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = nt * 8 + cq + e;
+        float v = sfr[nt][e] * a.scale_log2;
+        if (blk * kBlk + t >= ctx) v = -FLT_MAX;
+        sfr[nt][e] = v;
+        mx = fmaxf(mx, v);
+      }
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mn = fmaxf(m0, mx);
+    const float alpha = exp2f(m0 - mn);
+    m0 = mn;
+    float ps = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float pv = sfr[nt][e] > -FLT_MAX ? exp2f(sfr[nt][e] - mn) : 0.f;
+        sfr[nt][e] = pv;
+        ps += pv;
+      }
+    }
+    l0 = l0 * alpha + ps;
+#pragma unroll
+    for (int nn = 0; nn < 16; ++nn) {
+      o[nn][0] *= alpha;
+      o[nn][1] *= alpha;
+    }
+    uint32_t pa[4];
+    pa[0] = pack_bf16(sfr[0][0], sfr[0][1]);
+    pa[1] = 0;
+    pa[2] = pack_bf16(sfr[1][0], sfr[1][1]);
+    pa[3] = 0;
+    const int valid = ctx - blk * kBlk;
+    if (valid < kBlk) {
+      uint16_t* vw = const_cast<uint16_t*>(vs);
+      for (int e = lane; e < (kBlk - valid) * (D / 8); e += 32) {
+        const int r = valid + e / (D / 8), c8 = e % (D / 8);
+        *reinterpret_cast<uint4*>(vw + r * kRowPad + c8 * 8) = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int np = 0; np < 8; ++np) {
+      uint32_t v0, v1, v2, v3;
+      const uint16_t* p = vs + ((lm & 1) * 8 + lr) * kRowPad + np * 16 + (lm >> 1) * 8;
+      ldsm_x4_t(v0, v1, v2, v3, p);
+      mma_bf16(o[2 * np], pa, v0, v1);
+      mma_bf16(o[2 * np + 1], pa, v2, v3);
+    }
+    __syncwarp();
+    seg_advance(pre, B, kv, cc);
+  }
+  cp_async_wait<0>();
+  end_segment(seg);
+}
+
 static int attn_impl() {
   static int impl = -1;
   if (impl < 0) {
     const char* e = getenv("TF_ATTN_IMPL");
-    impl = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 3;
+    impl = (e && e[0] >= '1' && e[0] <= '4') ? e[0] - '0' : 4;
   }
   return impl;
 }
@@ -806,10 +1087,39 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
   *bps = per;
 }
 
+static bool use_v4(int D, int G, int B) { return attn_impl() == 4 && D == 128 && G <= 8 && B <= kV4MaxB; }
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static int64_t v4_kmax(int max_ctx) { return (std::max(1, (max_ctx + kBlk - 1) / kBlk) + kPerMin - 1) / kPerMin + 1; }
+
+static int64_t v4_counter_bytes(int B, int kv) { return ((int64_t)B * kv * 4 + 255) / 256 * 256; }
+
 template <int D, int G>
 static int launch(const AttnArgs& a, int B, cudaStream_t st) {
+  if (use_v4(D, G, B)) {
+    constexpr int GG = G <= 8 ? G : 8;
+    const int smem = kV4Warps * kV4Stages * 2 * kBlk * kRowPad * 2;
+    static bool attr4 = false;
+    if (!attr4) {
+      TF_CUDA(cudaFuncSetAttribute(paged_attn_stream_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr4 = true;
+    }
+    paged_attn_stream_kernel<GG><<<sm_count() * kV4CtasPerSm, kV4Warps * 32, smem, st>>>(a);
+    TF_LAUNCH_CHECK();
+    return TF_OK;
+  }
   dim3 grid(a.splits, B * a.kv_heads);
-  if (attn_impl() == 3 && D == 128 && G <= 8) {
+  if (attn_impl() >= 3 && D == 128 && G <= 8) {
     const int smem = kV3Warps * kV3Stages * 2 * kBlk * kRowPad * 2;
     static bool attr3 = false;
     if (!attr3) {
@@ -846,6 +1156,11 @@ extern "C" {
 int64_t tf_paged_decode_attn_workspace(int64_t pool, int32_t B, int32_t max_ctx, int32_t n_q_heads) {
   Pool* p = get_pool(pool);
   if (!p) return -1;
+  if (n_q_heads % p->kv_heads) return -1;
+  const int G = n_q_heads / p->kv_heads;
+  if (use_v4(p->head_dim, G, B))
+    return v4_counter_bytes(B, p->kv_heads) +
+           (int64_t)B * p->kv_heads * v4_kmax(max_ctx) * G * (p->head_dim + 2) * (int64_t)sizeof(float);
   int splits, bps;
   plan_splits(B, p->kv_heads, max_ctx, &splits, &bps);
   if (splits == 1) return 0;
@@ -878,15 +1193,31 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
   a.layer = layer;
   a.hq = n_q_heads;
   a.scale_log2 = scale * 1.4426950408889634f;
+  const int G = n_q_heads / p->kv_heads;
+  const int D = p->head_dim;
+  a.B = B;
+  if (use_v4(D, G, B)) {
+    a.kmax = (int32_t)v4_kmax(max_ctx);
+    const int64_t cb = v4_counter_bytes(B, p->kv_heads);
+    const int64_t need4 = cb + (int64_t)B * p->kv_heads * a.kmax * G * (D + 2) * (int64_t)sizeof(float);
+    TF_CHECK_ARG(workspace && workspace_bytes >= need4, "tf_paged_decode_attn: workspace too small (%lld < %lld)",
+                 (long long)workspace_bytes, (long long)need4);
+    a.counters = (int32_t*)workspace;
+    a.ws_ml = (float*)((char*)workspace + cb);
+    a.ws_acc = a.ws_ml + (int64_t)B * p->kv_heads * a.kmax * G * 2;
+    a.splits = 1;
+    a.blocks_per_split = 0;
+  } else {
   plan_splits(B, p->kv_heads, max_ctx, &a.splits, &a.blocks_per_split);
   int64_t need = a.splits == 1 ? 0 : (int64_t)B * n_q_heads * a.splits * (p->head_dim + 2) * (int64_t)sizeof(float);
   TF_CHECK_ARG(workspace_bytes >= need && (need == 0 || workspace), "tf_paged_decode_attn: workspace too small (%lld < %lld)",
                (long long)workspace_bytes, (long long)need);
   a.ws_acc = (float*)workspace;
   a.ws_ml = a.ws_acc + (int64_t)B * n_q_heads * a.splits * p->head_dim;
+  a.counters = nullptr;
+  a.kmax = 0;
+  }
   cudaStream_t st = (cudaStream_t)stream;
-  const int G = n_q_heads / p->kv_heads;
-  const int D = p->head_dim;
   if (D == 128 && G == 4) return launch<128, 4>(a, B, st);
   if (D == 128 && G == 5) return launch<128, 5>(a, B, st);
   if (D == 128 && G == 8) return launch<128, 8>(a, B, st);

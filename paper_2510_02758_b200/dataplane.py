@@ -131,8 +131,14 @@ class GpuDataPlane:
             self.s_compute = self.s_evict = self.s_load = torch.cuda.Stream(device=dev)
         else:
             self.s_compute = torch.cuda.Stream(device=dev)
-            self.s_evict = torch.cuda.Stream(device=dev)
-            self.s_load = torch.cuda.Stream(device=dev)
+            # copy streams at high priority: the SM swap kernel (partial-block
+            # edges of the auto engine) gets SMs as soon as running compute CTAs
+            # retire, instead of queueing behind a whole prefill / decode step -
+            # otherwise a load's measured rate collapses to the prefill's
+            # duration and the policy's t_io estimate (kvstore.py:173-193)
+            # tips every restore towards recompute
+            self.s_evict = torch.cuda.Stream(device=dev, priority=-1)
+            self.s_load = torch.cuda.Stream(device=dev, priority=-1)
         self._pending_table = []  # (row, lb, block) not yet applied on device
         self._appending = {}  # rid -> position reserved by the in-flight decode step
         self._d2h_busy = None  # (rid, lo, hi, kind, event)
@@ -144,7 +150,7 @@ class GpuDataPlane:
                       "fill_tokens": 0, "attn_launches": 0, "decode_steps": 0}
         self._events = []  # (kind, tokens, start_evt, end_evt) for measured transfer rates
         ws = max(1, int(lib.tf_paged_decode_attn_workspace(pool.handle, max(1, len(reqs)), self.max_len, 64)))
-        self._attn_ws = torch.empty(ws, dtype=torch.uint8, device=dev)
+        self._attn_ws = torch.zeros(ws, dtype=torch.uint8, device=dev)
         self.attn_out = None
 
     def enable_fused_write_through(self):
@@ -506,7 +512,7 @@ class GpuDataPlane:
         out = torch.empty_like(q)
         ws_need = int(lib.tf_paged_decode_attn_workspace(self.pool.handle, B, max(pos) + 1, hq))
         if ws_need > self._attn_ws.numel():
-            self._attn_ws = torch.empty(ws_need, dtype=torch.uint8, device=self.pool.device)
+            self._attn_ws = torch.zeros(ws_need, dtype=torch.uint8, device=self.pool.device)
         scale = 1.0 / float(self.pool.D) ** 0.5
         with torch.cuda.stream(st):
             for layer in range(n_layers):

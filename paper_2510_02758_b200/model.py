@@ -81,7 +81,7 @@ class PagedDecoder:
         self.prompts = {}
         self._unresolved = {}  # rid -> (pinned buffer, column) of an in-flight prefill's t0/t1
         self.scale = 1.0 / math.sqrt(hd)
-        self._ws = torch.empty(1, dtype=torch.uint8, device=self.device)
+        self._ws = torch.zeros(1, dtype=torch.uint8, device=self.device)
         self.steps = 0
         self.attn_timing = None  # list -> (algorithmic bytes, start event, end event) per attention launch
         self._graphs = {}
@@ -228,7 +228,11 @@ class PagedDecoder:
                 nxt = self._decode_rows(dp, list(batch), toks.to(self.device, non_blocking=True), pos, st)
             dp.stats["attn_launches"] += self.s.n_layers
             host = torch.empty(len(batch), dtype=torch.long, pin_memory=True)
-            host.copy_(nxt, non_blocking=True)  # sampled ids -> client (D2H of the step's result)
+            nxt = nxt.contiguous()
+            # sampled ids -> client (D2H of the step's result), zero-copy so the
+            # step's end event does not wait behind evict / write-through copies
+            check(lib.tf_copy_small(C.c_void_p(host.data_ptr()), C.c_void_p(nxt.data_ptr()), host.numel() * 8,
+                                    C.c_void_p(st.cuda_stream)), "tf_copy_small")
             self._last = (list(batch), host)
         self.steps += 1
 
@@ -255,7 +259,7 @@ class PagedDecoder:
             out = torch.empty_like(q)
             max_ctx = max(positions) + 1
             ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, self.hq)))
-            ws = torch.empty(ws_n, dtype=torch.uint8, device=self.device)
+            ws = torch.zeros(ws_n, dtype=torch.uint8, device=self.device)
             abytes = (sum(positions) + B) * 2 * self.hkv * s.head_dim * 2 + 2 * B * self.hq * s.head_dim * 2 \
                 + sum((p + 16) // 16 for p in positions) * 4
             res = []
@@ -296,7 +300,7 @@ class PagedDecoder:
             io[1].fill_(dp.scratch_row)
             stage = torch.zeros((3, Bp), dtype=torch.int64, pin_memory=True)
             ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, Bp, self._gmax_ctx, self.hq)))
-            ws = torch.empty(ws_n, dtype=torch.uint8, device=self.device)
+            ws = torch.zeros(ws_n, dtype=torch.uint8, device=self.device)
             with torch.cuda.stream(st):
                 self._forward_graphable(dp, io, Bp, ws, st)  # warm-up (kernel attributes, cuBLAS handles)
             st.synchronize()
@@ -323,7 +327,10 @@ class PagedDecoder:
         stage[2, :B] = torch.tensor(positions)
         stage[2, B:] = 0
         with torch.cuda.stream(st):
-            io.copy_(stage, non_blocking=True)
+            # zero-copy read of the pinned staging row (not a copy-engine H2D:
+            # those queue behind KV loads on the same engine)
+            check(lib.tf_copy_small(C.c_void_p(io.data_ptr()), C.c_void_p(stage.data_ptr()),
+                                    io.numel() * io.element_size(), C.c_void_p(st.cuda_stream)), "tf_copy_small")
             g.replay()
         # the staging buffer is reused next step only after this step completed
         return out[:B]
@@ -337,7 +344,7 @@ class PagedDecoder:
         max_ctx = max(positions) + 1
         need = int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, self.hq))
         if need > self._ws.numel():
-            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
         return self._layers_decode(dp, tokens, rows, pos32, ctx, B, max_ctx, self._ws, st, self.attn_timing,
                                    positions)
 

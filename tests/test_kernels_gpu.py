@@ -108,7 +108,7 @@ def _attn_case(cuda, B, ctx_list, L, H, HQ, D, layer):
     q = (torch.randn(B, HQ, D, device=cuda)).to(torch.bfloat16)
     out = torch.empty_like(q)
     ws_n = max(1, int(lib.lib.tf_paged_decode_attn_workspace(p.handle, B, max(ctx_list), HQ)))
-    ws = torch.empty(ws_n, dtype=torch.uint8, device=cuda)
+    ws = torch.zeros(ws_n, dtype=torch.uint8, device=cuda)
     lib.check(lib.lib.tf_paged_decode_attn(p.handle, C.c_void_p(q.data_ptr()), C.c_void_p(tab_d.data_ptr()), maxlb,
                                            C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B, max(ctx_list),
                                            layer, HQ, 1.0 / D ** 0.5, C.c_void_p(out.data_ptr()),
@@ -135,10 +135,47 @@ def _attn_case(cuda, B, ctx_list, L, H, HQ, D, layer):
     (5, [3, 64, 200, 513, 1000], 2, 2, 4, 64, 1),
     (3, [17, 900, 4096], 4, 8, 40, 128, 2),
     (1, [1], 2, 2, 4, 64, 0),
+    # stream-K (v4): many warps per long segment, many segments per warp, ragged
+    (64, [int(x) for x in np.random.default_rng(5).integers(1, 3000, 64)], 32, 8, 32, 128, 7),
+    (130, [16 * (i % 9) + 1 + i for i in range(130)], 4, 8, 64, 128, 3),
 ])
 def test_paged_attention_vs_fp32(cuda, case):
     worst = _attn_case(cuda, *case)
     assert worst <= 2e-2, worst  # bf16 output, fp32 accumulation (north-star tolerance)
+
+
+def test_paged_attention_workspace_reuse_is_deterministic(cuda):
+    """The stream-K merge counters reset themselves: relaunching with the same
+    workspace gives bit-identical outputs (merge order is fixed by slot)."""
+    lib = _lib()
+    B, L, H, HQ, D = 48, 2, 8, 32, 128
+    ctx_list = [int(x) for x in np.random.default_rng(9).integers(1, 2500, B)]
+    nblk_req = [(c + 15) // 16 for c in ctx_list]
+    p = _pool(cuda, sum(nblk_req) + 1, 1, L, H, D)
+    p.gpu.copy_((torch.randn(p.gpu.numel(), device=cuda) * 0.5).to(torch.bfloat16).view(torch.int16))
+    maxlb = max(nblk_req)
+    table = np.full((B, maxlb), -1, np.int32)
+    k = 0
+    for b in range(B):
+        table[b, : nblk_req[b]] = np.arange(k, k + nblk_req[b])
+        k += nblk_req[b]
+    tab_d = torch.from_numpy(table).to(cuda)
+    rows = torch.arange(B, dtype=torch.int32, device=cuda)
+    ctx = torch.tensor(ctx_list, dtype=torch.int32, device=cuda)
+    q = torch.randn(B, HQ, D, device=cuda).to(torch.bfloat16)
+    ws_n = max(1, int(lib.lib.tf_paged_decode_attn_workspace(p.handle, B, 4096, HQ)))
+    ws = torch.zeros(ws_n, dtype=torch.uint8, device=cuda)
+    outs = []
+    for _ in range(3):
+        out = torch.empty_like(q)
+        lib.check(lib.lib.tf_paged_decode_attn(p.handle, C.c_void_p(q.data_ptr()), C.c_void_p(tab_d.data_ptr()),
+                                               maxlb, C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B,
+                                               4096, 1, HQ, 1.0 / D ** 0.5, C.c_void_p(out.data_ptr()),
+                                               C.c_void_p(ws.data_ptr()), ws_n, None))
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+    p.close()
 
 
 def test_kv_append_writes_slots(cuda):
