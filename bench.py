@@ -205,6 +205,7 @@ def run_ours(args):
                 state["wall0"] = time.perf_counter()
                 state["ev0"] = len(dp._events)
                 state["pre0"], state["rc0"] = eng.total_preemptions, eng.total_recomputes
+                torch.cuda.nvtx.range_push("bench_timed")  # ncu --nvtx --nvtx-include bench_timed/
             return
         if state["phase"] == "timed":
             state["timed"].append(dict(rec))
@@ -213,10 +214,12 @@ def run_ours(args):
                 state["ev1"] = len(dp._events)
                 state["pre1"], state["rc1"] = eng.total_preemptions, eng.total_recomputes
                 state["phase"] = "done"
+                torch.cuda.nvtx.range_pop()
                 if not args.full_run:
                     eng._stop = True
 
-    eng = RealtimeEngine(tr, policy, cm, sim, dp, skip_idle=True, on_step=on_step, lockstep=lockstep)
+    eng = RealtimeEngine(tr, policy, cm, sim, dp, skip_idle=True, on_step=on_step, lockstep=lockstep,
+                         max_wall_s=args.max_wall if args.full_run else None)
     if args.watchdog:
         _start_watchdog(eng, dp, args.watchdog)
     if world > 1:
@@ -277,7 +280,7 @@ def run_ours(args):
         G = shape.n_q_heads // shape.n_kv_heads
         kname = {"1": "paged_attn_kernel (v1)", "2": "paged_attn_tma_kernel (v2)",
                  "3": f"paged_attn_mma_kernel<{G}> (v3) + combine"}.get(
-            os.environ.get("TF_ATTN_IMPL", "4")[:1], f"paged_attn_stream_kernel<{G}> (v4 stream-K, tensor cores)")
+            os.environ.get("TF_ATTN_IMPL", "3")[:1], f"paged_attn_stream_kernel<{G}> (v4 stream-K, tensor cores)")
         roof = {"bound": "hbm", "kernel": kname, "achieved": round(ach, 1),
                 "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
                 "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live),
@@ -336,15 +339,23 @@ def run_ours(args):
         "gpu_launches": None,
         "first_tokens_in_window": len(ttft),
     }
-    out["gpu_launches"] = int(len(timed) * shape.n_layers * (3 if args.graphs else 2) + len(xfers))
+    # this package's kernels per decode step: fused rope/append(+write-through) and
+    # paged attention per layer, the zero-copy step input / sampled-id copies;
+    # plus one swap launch per chunk (prefill jobs' kernels are not counted)
+    attn_per_layer = 2 if os.environ.get("TF_ATTN_IMPL", "3")[:1] in ("2", "3") else 1
+    out["gpu_launches"] = int(len(timed) * (shape.n_layers * (1 + attn_per_layer) + (2 if args.graphs else 0))
+                              + len(xfers))
     if args.full_run:
         from paper_2510_02758_b200.metrics import EffectiveThroughputConfig, effective_throughput
 
-        out["full_run"] = {"effective_tok_s": effective_throughput(res.records, res.total_time,
-                                                                   EffectiveThroughputConfig()),
-                           "ttft_latency": ttft_latency_stats(res.records), "total_time_s": res.total_time,
-                           "wall_s": eng.wall_s, "preemptions": res.total_preemptions,
-                           "recomputes": res.total_recomputes}
+        done = [r for r in res.records if r.gen_times]
+        out["full_run"] = {"truncated": eng.truncated, "requests_with_first_token": len(done),
+                           "ttft_latency": ttft_latency_stats(done) if done else None,
+                           "total_time_s": res.total_time, "wall_s": eng.wall_s,
+                           "preemptions": res.total_preemptions, "recomputes": res.total_recomputes}
+        if not eng.truncated:
+            out["full_run"]["effective_tok_s"] = effective_throughput(res.records, res.total_time,
+                                                                      EffectiveThroughputConfig())
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, timed, quick=True)
     if rank == 0:
@@ -485,6 +496,8 @@ def main():
     ap.add_argument("--fused-wt", type=int, default=1, help="mirror KV to the host inside the prefill/decode "
                     "epilogue (SURVEY 8f #1) instead of separate write-through chunks")
     ap.add_argument("--full-run", action="store_true")
+    ap.add_argument("--max-wall", type=float, default=600.0, help="--full-run: stop (truncated) after this many "
+                    "seconds of wall time")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-batch", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -158,7 +158,7 @@ def overlap(pool, args):
     q = torch.randn(B, HQ, 128, device=dev).to(torch.bfloat16)
     out = torch.empty_like(q)
     ws_n = max(1, int(_lib.lib.tf_paged_decode_attn_workspace(pool.handle, B, ctx, HQ)))
-    ws = torch.empty(ws_n, dtype=torch.uint8, device=dev)
+    ws = torch.zeros(ws_n, dtype=torch.uint8, device=dev)
     sc, sd, sh = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     # swap traffic smaller than one decode's time (so 100% hiding is possible):
     # NB blocks out (write-through + evict) and NB in (loads), 2 MiB each

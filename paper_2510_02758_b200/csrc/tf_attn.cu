@@ -877,11 +877,33 @@ __global__ void __launch_bounds__(kV4Warps * 32, kV4CtasPerSm) paged_attn_stream
   const int64_t tile = (int64_t)kBlk * D;
   SegCursor ic;  // issue cursor (runs two blocks ahead of the compute cursor)
   seg_locate(pre, B, kv, lo, ic);
+  const int32_t* itrow = a.table + (int64_t)a.rows[ic.b] * a.stride;  // table row of ic.b
+  int itrow_b = ic.b;
+  const int r0q = lane >> 2, cqq = (lane & 3) * 2;
+  uint32_t qn[8][2];  // q fragments of the next segment, prefetched at its first issue
+  auto load_q = [&](int b, int kvh) {
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t qlo = 0, qhi = 0;
+      if (r0q < G) {
+        const uint16_t* qrow = a.q + ((int64_t)b * a.hq + kvh * G + r0q) * D + kk * 16 + cqq;
+        qlo = __ldg(reinterpret_cast<const unsigned int*>(qrow));
+        qhi = __ldg(reinterpret_cast<const unsigned int*>(qrow + 8));
+      }
+      qn[kk][0] = qlo;
+      qn[kk][1] = qhi;
+    }
+  };
+  load_q(ic.b, ic.kvh);
   auto issue = [&](int i) {
     if (i < n) {
+      if (ic.b != itrow_b) {
+        itrow_b = ic.b;
+        itrow = a.table + (int64_t)a.rows[ic.b] * a.stride;
+      }
       const int64_t koff = (((int64_t)a.layer * 2 + 0) * kv + ic.kvh) * tile;
       const int64_t voff = (((int64_t)a.layer * 2 + 1) * kv + ic.kvh) * tile;
-      const int64_t base = (int64_t)__ldg(a.table + (int64_t)a.rows[ic.b] * a.stride + ic.j) * a.block_elems;
+      const int64_t base = (int64_t)__ldg(itrow + ic.j) * a.block_elems;
       uint16_t* ks = ring + (i % kV4Stages) * 2 * kTileElems;
       uint16_t* vs = ks + kTileElems;
 #pragma unroll
@@ -910,15 +932,9 @@ __global__ void __launch_bounds__(kV4Warps * 32, kV4CtasPerSm) paged_attn_stream
   auto begin_segment = [&]() {
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      uint32_t qlo = 0, qhi = 0;
-      if (r0 < G) {
-        const uint16_t* qrow = a.q + ((int64_t)cc.b * a.hq + cc.kvh * G + r0) * D + kk * 16 + cq;
-        qlo = *reinterpret_cast<const uint32_t*>(qrow);
-        qhi = *reinterpret_cast<const uint32_t*>(qrow + 8);
-      }
-      qa[kk][0] = qlo;
+      qa[kk][0] = qn[kk][0];
       qa[kk][1] = 0;
-      qa[kk][2] = qhi;
+      qa[kk][2] = qn[kk][1];
       qa[kk][3] = 0;
     }
 #pragma unroll
@@ -927,6 +943,11 @@ __global__ void __launch_bounds__(kV4Warps * 32, kV4CtasPerSm) paged_attn_stream
     l0 = 0.f;
     ctx = a.ctx[cc.b];
     seg = cc;
+    // prefetch the next segment's q (used at the next boundary, >= 1 block later)
+    SegCursor nx = cc;
+    nx.j = nx.nb - 1;
+    seg_advance(pre, B, kv, nx);
+    if (nx.b < B) load_q(nx.b, nx.kvh);
   };
 
   auto end_segment = [&](const SegCursor& sc) {
@@ -965,19 +986,50 @@ __global__ void __launch_bounds__(kV4Warps * 32, kV4CtasPerSm) paged_attn_stream
     old = __shfl_sync(0xffffffffu, old, 0);
     const int cnt = last - first + 1;
     if (old != cnt - 1) return;
-    // last of the segment's warps: merge the cnt partials
+    // last of the segment's warps: merge the cnt partials.  Lane l owns
+    // elements [l*E, l*E+E) of the [G][D] tile (E = 4G, whole float4s, never
+    // straddling a row); all loads of a pass are independent (one L2 round trip).
     __threadfence();
-    for (int e = lane; e < G * D; e += 32) {
-      const int g = e / D, d = e % D;
-      float mm = -FLT_MAX;
-      for (int k = 0; k < cnt; ++k) mm = fmaxf(mm, __ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2));
-      float ll = 0.f, aa = 0.f;
-      for (int k = 0; k < cnt; ++k) {
-        const float f = exp2f(__ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2) - mm);
-        ll += __ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2 + 1) * f;
-        aa += __ldcg(a.ws_acc + ((slot0 + k) * G + g) * D + d) * f;
+    constexpr int E = G * D / 32;
+    constexpr int NC = E / 4;
+    float mrow[NC], lsum[NC];
+    float4 acc4[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      mrow[c] = -FLT_MAX;
+      lsum[c] = 0.f;
+      acc4[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int k = 0; k < cnt; ++k) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int g = (lane * E + 4 * c) / D;
+        mrow[c] = fmaxf(mrow[c], __ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2));
       }
-      a.out[(row0 + g) * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(ll > 0.f ? aa / ll : 0.f));
+    }
+    for (int k = 0; k < cnt; ++k) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int e = lane * E + 4 * c, g = e / D, d = e % D;
+        const float mk = __ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2);
+        const float lk = __ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2 + 1);
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.ws_acc + ((slot0 + k) * G + g) * D + d));
+        const float w = exp2f(mk - mrow[c]);
+        lsum[c] += lk * w;
+        acc4[c].x += v.x * w;
+        acc4[c].y += v.y * w;
+        acc4[c].z += v.z * w;
+        acc4[c].w += v.w * w;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int e = lane * E + 4 * c, g = e / D, d = e % D;
+      const float inv = lsum[c] > 0.f ? 1.f / lsum[c] : 0.f;
+      uint2 pk;
+      pk.x = pack_bf16(acc4[c].x * inv, acc4[c].y * inv);
+      pk.y = pack_bf16(acc4[c].z * inv, acc4[c].w * inv);
+      *reinterpret_cast<uint2*>(a.out + (row0 + g) * D + d) = pk;
     }
     if (lane == 0) a.counters[seg] = 0;  // ready for the next launch
   };
@@ -1069,7 +1121,7 @@ static int attn_impl() {
   static int impl = -1;
   if (impl < 0) {
     const char* e = getenv("TF_ATTN_IMPL");
-    impl = (e && e[0] >= '1' && e[0] <= '4') ? e[0] - '0' : 4;
+    impl = (e && e[0] >= '1' && e[0] <= '4') ? e[0] - '0' : 3;
   }
   return impl;
 }

@@ -382,7 +382,7 @@ class GpuDataPlane:
         self._last_d2h_event[rid] = t1
         self.stats["d2h_tokens"] += ch.tokens
         self.stats["d2h_launches"] += 1
-        return t1
+        return t0, t1
 
     def d2h_done(self, ch, alive):
         rid, lo, hi, kind, ev = self._d2h_busy
@@ -409,6 +409,8 @@ class GpuDataPlane:
         if self.mode == "realtime" and ev is not None:
             st.wait_event(ev)
         segs = self._segments(rid, miss)
+        if self.swap_engine != _lib.ENGINE_SM:
+            segs = self._widen_loads(rid, segs, miss)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(st)
@@ -420,7 +422,28 @@ class GpuDataPlane:
         self.stats["h2d_launches"] += 1
         # realtime: the request turns RUNNING only after the engine observed
         # every load chunk complete, so decode needs no wait on this stream
-        return t1
+        return t0, t1
+
+    def _widen_loads(self, rid, segs, miss):
+        """A partial-block load whose block holds nothing else (no other slot
+        LIVE / RESERVED / DETACHED) is issued as the whole block: one
+        contiguous run on the copy engines instead of 2*kv_heads*layers short
+        runs for the SM kernel, which would have to wait for SMs behind the
+        compute stream.  The extra slots carry host bytes no one reads (they
+        lie beyond the request's context, or are refilled before use)."""
+        f, tab = self.flags[rid], self.gtab[rid]
+        loading = np.zeros(len(f), bool)
+        loading[miss] = True
+        out = []
+        for g, h, s0, n in segs:
+            if n < self.B:
+                j = int(np.nonzero(tab == g)[0][0])
+                lo, hi = j * self.B, (j + 1) * self.B
+                others = (f[lo:hi] & (LIVE | RESERVED | DETACHED)).astype(bool) & ~loading[lo:hi]
+                if not others.any():
+                    s0, n = 0, self.B
+            out.append((g, h, s0, n))
+        return out
 
     def release_prefix(self, rid, n):
         f = self.flags[rid]

@@ -47,9 +47,11 @@ from .engine import (
 
 class RealtimeEngine(Engine):
     def __init__(self, trace, policy, cm, sim, dataplane, skip_idle: bool = True, on_step=None, max_steps=None,
-                 lockstep=None):
+                 lockstep=None, max_wall_s=None):
         super().__init__(trace, policy, cm, sim, dataplane)
         self.lockstep = lockstep
+        self.max_wall_s = max_wall_s  # stop (truncated) after this much wall time
+        self.truncated = False
         assert dataplane is not None and dataplane.mode == "realtime"
         self.skip_idle = skip_idle
         self.on_step = on_step  # callback(record dict) after every decode iteration
@@ -106,9 +108,10 @@ class RealtimeEngine(Engine):
                     if self.state[rid].status == PREFILL_WAIT:
                         self.state[rid].status = PREFILLING
                 self._mem_acquire(need)
+                ev0 = self.dp.record_event()
                 self.dp.fill_start(job, self)
                 self.gpu_job = job
-                self._gpu = ("prefill", job, start, self._end_event())
+                self._gpu = ("prefill", job, start, self._end_event(), ev0)
                 return
         chosen = self._decode_candidates()
         if not chosen:
@@ -119,9 +122,10 @@ class RealtimeEngine(Engine):
         if not chosen:
             return
         batch = tuple(chosen)
+        ev0 = self.dp.record_event()
         self.dp.decode_start(batch, self)
         self.gpu_job = ("decode", batch)
-        self._gpu = ("decode", batch, start, self._end_event())
+        self._gpu = ("decode", batch, start, self._end_event(), ev0)
 
     def _end_event(self):
         return self.dp.record_event()
@@ -139,42 +143,57 @@ class RealtimeEngine(Engine):
         ch_.queue.popleft()
         ch_.in_service = head
         ch_.started = time_
-        ev = (self.dp.d2h_start if ch_.direction == "d2h" else self.dp.h2d_start)(head, self)
-        self._lanes[ch_.direction] = (time_, ev)
+        ev0, ev1 = (self.dp.d2h_start if ch_.direction == "d2h" else self.dp.h2d_start)(head, self)
+        self._lanes[ch_.direction] = (time_, ev1, ev0)
 
     # ------------------------------------------------------------------- loop
     def _poll_completions(self):
-        """-> (progressed, clock).  Lockstep: completions and clock agreed over ranks."""
-        slots = (("gpu", self._gpu, 3, 0), ("d2h", self._lanes["d2h"], 1, 1), ("h2d", self._lanes["h2d"], 1, 1))
-        flags, times = [], []
-        for what, v, i, _ in slots:
-            ok = v is not None and v[i].query()
+        """-> (progressed, clock).  A job's duration is its DEVICE span (start
+        event recorded just before its launch .. end event), so host lag in
+        issuing it (e.g. while Python enqueues a long prefill) is not charged to
+        the job - the measured rates that feed update_rate_ema / the policy's
+        t_io (kvstore.py:173-193, :255-259) see only the transfer itself.
+        Lockstep: done flags, end and start times and the clock are agreed
+        over the TP ranks."""
+        slots = (("gpu", self._gpu, 0), ("d2h", self._lanes["d2h"], 1), ("h2d", self._lanes["h2d"], 1))
+        flags, ends, starts = [], [], []
+        for what, v, _ in slots:
+            # v = (host start time, end event, start event)
+            ok = v is not None and v[1 if what != "gpu" else 3].query()
             flags.append(ok)
-            t = self._event_time(v[i]) if ok else 0.0
-            times.append(max(t, v[0]) if ok and what != "gpu" else t)
+            if ok:
+                e_end, e_start = (v[3], v[4]) if what == "gpu" else (v[1], v[2])
+                st = max(v[2] if what == "gpu" else v[0], self._event_time(e_start))
+                starts.append(st)
+                ends.append(max(self._event_time(e_end), st))
+            else:
+                starts.append(0.0)
+                ends.append(0.0)
         clock = self._clock()
         if self.lockstep is not None:
-            clock, flags, times = self.lockstep.agree(clock, flags, times)
-        done = [(t, order, what) for (what, _, _, order), ok, t in zip(slots, flags, times) if ok]
+            clock, flags, ends, starts = self.lockstep.agree(clock, flags, ends, starts)
+        done = [(t, order, what, s0) for (what, _, order), ok, t, s0 in zip(slots, flags, ends, starts) if ok]
         if not done:
             return False, clock
         done.sort()
-        for t, _, what in done:
+        for t, _, what, s0 in done:
             self.now = max(self.now, t)
             if what == "gpu":
-                kind, payload, start, _ = self._gpu
+                kind, payload = self._gpu[0], self._gpu[1]
                 self._gpu = None
-                dur = max(t - start, 1e-9)
-                self.jobs.append((kind, start, t, dur))
+                dur = max(t - s0, 1e-9)
+                self.jobs.append((kind, s0, t, dur))
                 if kind == "prefill":
                     self._on_prefill_done(t, min(payload.members), payload, dur)
                 else:
                     n_before = len(self.steps)
-                    self._record_step(payload, start, t, dur)
+                    self._record_step(payload, s0, t, dur)
                     self._on_decode_iter_done(t, min(payload), payload, dur)
                     self._finish_step(n_before)
             else:
                 self._lanes[what] = None
+                ch_ = self.d2h if what == "d2h" else self.h2d
+                ch_.started = max(ch_.started, s0)
                 self._on_chunk_transfer_done(t, -1, what)
         return True, clock
 
@@ -209,6 +228,9 @@ class RealtimeEngine(Engine):
         wall0 = time.perf_counter()
         idle_spins = 0
         while self.live > 0 and not self._stop:
+            if self.max_wall_s is not None and time.perf_counter() - wall0 > self.max_wall_s:
+                self.truncated = True
+                break
             progressed, now = self._poll_completions()
             while self._heap and self._heap[0][0] <= now:
                 t, _, subject, seq = heapq.heappop(self._heap)

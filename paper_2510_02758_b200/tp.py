@@ -10,7 +10,7 @@ Two collectives, nothing else:
 * data path: one NCCL all-reduce (sum) after o_proj and one after down_proj
   per layer (B x hidden bf16 each), on the compute stream
   (``model.PagedDecoder`` with ``tp=TpGroup(...)``);
-* control path: ``Lockstep.agree`` - one 7-double all-reduce (max) per loop
+* control path: ``Lockstep.agree`` - one 10-double all-reduce (max) per loop
   iteration of the real-time engine over a CPU (gloo) group.  Instead of
   broadcasting rank 0's decisions, every rank runs the same deterministic
   engine and bit-exact GPU selector on the same agreed event sequence: a
@@ -37,17 +37,22 @@ class Lockstep:
         self.world = dist.get_world_size(group)
         self.calls = 0
 
-    def agree(self, clock: float, flags, times):
-        v = np.empty(7, dtype=np.float64)
+    def agree(self, clock: float, flags, ends, starts):
+        """-> (clock, flags, ends, starts) agreed over the ranks: an item is
+        done iff done on every rank; its end / start is the latest rank's."""
+        k = len(flags)
+        v = np.empty(1 + 3 * k, dtype=np.float64)
         v[0] = clock
-        for i in range(3):
+        for i in range(k):
             # max-reduction of (1 - done): an item is done only if done everywhere
             v[1 + i] = 0.0 if flags[i] else 1.0
-            v[4 + i] = times[i] if flags[i] else -math.inf
+            v[1 + k + i] = ends[i] if flags[i] else -math.inf
+            v[1 + 2 * k + i] = starts[i] if flags[i] else -math.inf
         t = torch.from_numpy(v)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         self.calls += 1
-        return float(v[0]), [v[1 + i] == 0.0 for i in range(3)], [float(v[4 + i]) for i in range(3)]
+        return (float(v[0]), [v[1 + i] == 0.0 for i in range(k)], [float(v[1 + k + i]) for i in range(k)],
+                [float(v[1 + 2 * k + i]) for i in range(k)])
 
     def same(self, text: str) -> bool:
         """True iff every rank holds the same ``text`` (e.g. the event hash)."""

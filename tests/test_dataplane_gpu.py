@@ -186,3 +186,42 @@ def test_attention_inside_engine_matches_fp32(cuda):
             worst = max(worst, float(np.abs(got - ref).max()))
     # bf16 output of fp32-accumulated attention: max-abs 2e-2 relative to fp32 (north star)
     assert worst <= 2e-2, worst
+
+
+@pytest.mark.parametrize("name", ["c2_burst256_s1_tokenflow"])
+def test_c2_replay_parity_full_size(name, cuda):
+    """C2 at full size (256 requests, 163,840-token ledger, 11,392-block pool):
+    the GPU selector + GPU data plane reproduce the reference's event hash,
+    decisions and chunk sequence, and every block / host table transition
+    equals the CPU restatement's (KV tensors use the tiny 2-layer shape here -
+    tables and chunk bytes do not depend on it)."""
+    import hashlib
+    import json
+
+    from paper_2510_02758_b200.costs import CostModel
+    from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
+    from paper_2510_02758_b200.engine import Engine, SimConfig
+    from paper_2510_02758_b200.scheduler import SchedulerConfig, make_policy
+    from paper_2510_02758_b200.workload import load_trace
+
+    g = load_golden("runs", name)
+    tr = load_trace(trace_path(g["trace"]))
+    nb = pool_blocks(g["sim"], len(tr.requests))
+    nh = g["sim"]["cpu_mem_tokens"] // 16 + len(tr.requests)
+    pool = KvPool(nb, nh, n_layers=2, kv_heads=2, head_dim=64, device=cuda)
+    gpu = GpuDataPlane(tr.requests, pool, mode="replay", attention="all", n_q_heads=4)
+    cpu = CpuDataPlane(tr.requests, nb, nh, 2, 2, 64)
+    tee = Tee(gpu, cpu, check_every=10 ** 9)
+    eng = Engine(tr, make_policy(g["policy"], SchedulerConfig(**g["sched"])), CostModel(**g["cm"]),
+                 SimConfig(**g["sim"]), dataplane=tee)
+    res = eng.run()
+    assert res.event_hash() == g["event_hash"]
+    assert res.decision_log == g["decision_log"]
+    h = hashlib.sha256()
+    for r in res.chunk_rows():
+        h.update(json.dumps(r, separators=(",", ":"), sort_keys=True).encode())
+        h.update(b"\n")
+    assert h.hexdigest() == g["chunk_hash"]
+    assert res.total_preemptions == g["total_preemptions"] and res.total_recomputes == g["total_recomputes"]
+    tee.compare_bytes(eng)
+    pool.close()

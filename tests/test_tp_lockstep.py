@@ -47,10 +47,10 @@ class TimedPlane:
         cost *= 1.0 + self.jitter * (2 * self.rng.random() - 1)
         start = max(time.perf_counter(), self.busy[lane])
         self.busy[lane] = start + cost
-        return FakeEvent(self.busy[lane])
+        return FakeEvent(start), FakeEvent(self.busy[lane])
 
     def record_event(self):
-        return FakeEvent(max(time.perf_counter(), self.busy["c"]))
+        return FakeEvent(max(time.perf_counter(), self.busy["c"]))  # the compute lane's current tail
 
     def fill_start(self, job, eng):
         self._run("c", 2e-3 + 2e-6 * sum(job.reserve.values()))
