@@ -271,7 +271,8 @@ def run_ours(args):
     hbm, peak_kind = _peaks()
     roof = None
     big = max(timed, key=lambda r: r["batch"])
-    live = [r for r in big["rids"] if eng.state[r].status == "running"]
+    # (a --full-run has served the whole trace by now: no live batch left to probe)
+    live = [] if args.full_run else [r for r in big["rids"] if eng.state[r].status == "running"]
     if live:
         per = model.measure_attention(dp, live, [eng.state[r].kv.total_kv - 1 for r in live])
         avg_ms = sum(ms for _, ms in per) / len(per)
@@ -493,8 +494,10 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c2", "c4"], help="c2: Llama3-8B replicas (C2/C3, default); "
                     "c4: Qwen2.5-32B tensor-parallel over the launched ranks")
     ap.add_argument("--graphs", type=int, default=1)
-    ap.add_argument("--fused-wt", type=int, default=1, help="mirror KV to the host inside the prefill/decode "
-                    "epilogue (SURVEY 8f #1) instead of separate write-through chunks")
+    ap.add_argument("--fused-wt", type=int, default=0, help="1: mirror KV to the host inside the prefill/decode "
+                    "epilogue (SURVEY 8f #1) instead of the reference's write-through chunks.  Off by default: it "
+                    "makes every preemption an instant full release, which tips the reference policy into "
+                    "preempt/recompute churn on the C2 burst (DESIGN.md section 7)")
     ap.add_argument("--full-run", action="store_true")
     ap.add_argument("--max-wall", type=float, default=600.0, help="--full-run: stop (truncated) after this many "
                     "seconds of wall time")
