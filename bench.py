@@ -186,6 +186,27 @@ def run_ours(args):
         dp.enable_scratch()
         model.enable_graphs(dp)
     policy = BufferAwarePolicy(c2.sched_cfg(SchedulerConfig))
+    tick_dump = []
+    if args.dump_ticks:
+        import dataclasses
+
+        lo_t, hi_t = (float(x) for x in args.dump_window.split(","))
+        orig_tick = policy.on_tick
+
+        def on_tick(view):
+            dec = orig_tick(view)
+            if lo_t <= view.now <= hi_t:
+                snap = {k: getattr(view, k) for k in ("now", "free_slots", "gpu_mem_free", "gpu_mem_total",
+                                                      "cpu_mem_total", "max_batch", "gamma", "prefill_s_per_token",
+                                                      "offload_enabled", "h2d_blocked_tokens")}
+                snap["members"] = [dataclasses.asdict(m) for m in view.members]
+                snap["waiting"] = [dataclasses.asdict(w) for w in view.waiting]
+                tick_dump.append({"snapshot": snap, "mode": dec.mode, "preempt": list(dec.preempt),
+                                  "resume": [list(r) for r in dec.resume],
+                                  "prefill_batches": [list(b) for b in dec.prefill_batches]})
+            return dec
+
+        policy.on_tick = on_tick
     sim = c2.sim_cfg(SimConfig, debug_checks=False)
     cm = c2.cost_model(CostModel)
 
@@ -282,8 +303,10 @@ def run_ours(args):
         kname = {"1": "paged_attn_kernel (v1)", "2": "paged_attn_tma_kernel (v2)",
                  "3": f"paged_attn_mma_kernel<{G}> (v3) + combine"}.get(
             os.environ.get("TF_ATTN_IMPL", "3")[:1], f"paged_attn_stream_kernel<{G}> (v4 stream-K, tensor cores)")
+        traffic, tsrc = _ncu_traffic(avg_bytes)
         roof = {"bound": "hbm", "kernel": kname, "achieved": round(ach, 1),
-                "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
+                "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                "traffic": traffic, "traffic_source": tsrc,
                 "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live),
                 "algorithmic_bytes_per_launch": round(avg_bytes),
                 "note": f"bytes = sum(ctx) x {pool.H * pool.D * 4} B (K+V, {pool.H} kv heads x {pool.D} x bf16) + "
@@ -357,6 +380,11 @@ def run_ours(args):
         if not eng.truncated:
             out["full_run"]["effective_tok_s"] = effective_throughput(res.records, res.total_time,
                                                                       EffectiveThroughputConfig())
+    if args.dump_ticks:
+        import gzip
+
+        with gzip.open(args.dump_ticks, "wt") as f:
+            json.dump({"ticks": tick_dump, "decision_log": res.decision_log}, f)
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, timed, quick=True)
     if rank == 0:
@@ -366,6 +394,25 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return out
+
+
+def _ncu_traffic(alg_bytes):
+    """DRAM bytes per launch for the attention kernel: the DRAM-traffic /
+    algorithmic-bytes ratio of the committed ncu --set full capture of the
+    same kernel (profiles/r1_attn_ncu_v3_v4.json) at the closest launch size,
+    applied to this launch's algorithmic bytes."""
+    p = ROOT / "profiles" / "r1_attn_ncu_v3_v4.json"
+    impl = os.environ.get("TF_ATTN_IMPL", "3")[:1]
+    want = "stream" if impl == "4" else "mma"
+    try:
+        caps = [k for k in json.loads(p.read_text())["kernels"] if want in k["kernel"]]
+    except (OSError, ValueError, KeyError):
+        return None, None
+    if not caps:
+        return None, None
+    k = min(caps, key=lambda c: abs(math.log(c["algorithmic_bytes"] / alg_bytes)))
+    return int(k["traffic_over_algorithmic"] * alg_bytes), (
+        f"ncu --set full capture {k['capture']}: dram read+write / algorithmic = {k['traffic_over_algorithmic']}")
 
 
 def _start_watchdog(eng, dp, period):
@@ -506,6 +553,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--watchdog", type=float, default=0.0, help="debug: dump engine state every N seconds")
+    ap.add_argument("--dump-ticks", default=None, help="debug: gzip JSON of the policy's snapshots + decisions")
+    ap.add_argument("--dump-window", default="0,1e9", help="debug: virtual-time window of --dump-ticks")
     args = ap.parse_args()
     if args.host_blocks <= 0:
         args.host_blocks = 26000 if args.full_run else 16384

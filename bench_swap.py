@@ -123,7 +123,7 @@ def sweep(args):
                 print(json.dumps(rows[-1]), flush=True)
         n *= 2
     # bit-exact round trip at the largest size, SM engine
-    k = min(args.max_blocks, args.host_blocks)
+    k = min(args.max_blocks, args.host_blocks, 4096)
     g = perm[:k]
     pool.gpu.view(args.max_blocks, -1)[torch.from_numpy(g).to(dev)] = torch.randint(
         -30000, 30000, (k, pool.block_elems), dtype=torch.int16, device=dev)

@@ -13,6 +13,7 @@
 // G=Hq/Hkv query heads' scores with a butterfly reduce-scatter (30 shuffles
 // instead of 128), and accumulates P.V in fp32.
 #include <float.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -1131,8 +1132,16 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
   const int base = std::max(1, B * kv_heads);
   // >= ~4 waves of resident CTAs (3 per SM) so the tail wave is cheap,
   // >= 8 blocks per split so the pipeline prologue is amortised
-  const int target = attn_impl() >= 2 ? 148 * 2 * 4 : 148 * 6;  // v2/v3 run 2 CTAs per SM
-  int s = std::max(1, std::min((target + base - 1) / base, (nblk + 7) / 8));
+  // tuning knobs (TF_ATTN_WAVES, TF_ATTN_MINBLK) for the split planner
+  static int waves = -1, minblk = -1;
+  if (waves < 0) {
+    const char* w = getenv("TF_ATTN_WAVES");
+    const char* m = getenv("TF_ATTN_MINBLK");
+    waves = w ? std::max(1, atoi(w)) : 4;
+    minblk = m ? std::max(1, atoi(m)) : 8;
+  }
+  const int target = attn_impl() >= 2 ? 148 * 2 * waves : 148 * 6;  // v2/v3 run 2 CTAs per SM
+  int s = std::max(1, std::min((target + base - 1) / base, (nblk + minblk - 1) / minblk));
   int per = (nblk + s - 1) / s;
   s = (nblk + per - 1) / per;
   *splits = s;

@@ -79,6 +79,8 @@ def main():
     ap.add_argument("--out", default="gpurun_out/attn_bench.json")
     ap.add_argument("--only", default=None, help="B:ctx:plan, e.g. 64:ragged500-3000:exact (one case, for ncu)")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--batches", default="32,64,96,128")
+    ap.add_argument("--plans", default="exact,pool")
     args = ap.parse_args()
     dev = torch.device("cuda")
     pool = KvPool(22000, 1, 32, 8, 128, device=dev)
@@ -86,11 +88,11 @@ def main():
     pk = peak()
     rng = np.random.default_rng(0)
     cases = []
-    for B in (32, 64, 96, 128):
+    for B in [int(x) for x in args.batches.split(",")]:
         for name, ctxs in (("uniform2600", [2600] * B),
                            ("ragged500-3000", list(rng.integers(500, 3000, B))),
                            ("short736", list(rng.integers(600, 870, B)))):
-            for plan in ("exact", "pool"):
+            for plan in args.plans.split(","):
                 if args.only and args.only != f"{B}:{name}:{plan}":
                     continue
                 plan_ctx = max(ctxs) if plan == "exact" else 4096
