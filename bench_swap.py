@@ -141,10 +141,46 @@ def sweep(args):
            "roundtrip_bit_exact_blocks": k if ok else -1, "rows": rows}
     if args.overlap:
         out["overlap"] = overlap(pool, args)
+    out["wt_chunks"] = wt_chunks(pool, args)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps(out, indent=1))
     print(json.dumps({k: v for k, v in out.items() if k != "rows"}))
     pool.close()
+
+
+def wt_chunks(pool, args):
+    """Write-through-shaped chunks: n tokens starting at slot 5 of a block
+    (unaligned, as the reference's write-through pointer is), gathered to the
+    host with each engine; per-chunk CUDA-event time -> algorithmic GB/s
+    (tokens x 128 KiB / time)."""
+    dev = pool.device
+    st = torch.cuda.Stream(priority=-1)
+    bpt = pool.block_bytes // pool.B
+    rows = []
+    for n in (8, 16, 32, 64, 128, 256, 512):
+        segs = []
+        pos, first = 5, 5
+        blk = 0
+        left = n
+        while left > 0:
+            k = min(left, 16 - pos % 16)
+            segs.append((blk, blk, pos % 16, k))
+            left -= k
+            pos += k
+            blk += 1
+        arr = (_lib.TfSeg * len(segs))()
+        for i, (g, h, s0, k) in enumerate(segs):
+            arr[i].gpu_block, arr[i].host_block, arr[i].slot_begin, arr[i].n_slots = g, h, s0, k
+        for eng in (0, 1, 2):
+            def go():
+                _lib.check(_lib.lib.tf_kv_gather_d2h(pool.handle, arr, len(segs), 0, pool.L, eng,
+                                                     C.c_void_p(st.cuda_stream)))
+            t = timed(go, st, reps=20)
+            rows.append({"tokens": n, "engine": {0: "sm", 1: "ce", 2: "auto"}[eng], "segments": len(segs),
+                         "us": round(t * 1e6, 2), "gbs": round(n * bpt / t / 1e9, 2)})
+            print(json.dumps(rows[-1]), flush=True)
+    del first, dev
+    return rows
 
 
 def overlap(pool, args):
@@ -211,8 +247,15 @@ def main():
     ap.add_argument("--overlap", action="store_true")
     ap.add_argument("--overlap-blocks", type=int, default=96)
     ap.add_argument("--out", default="gpurun_out/swap_sweep.json")
+    ap.add_argument("--wt-only", action="store_true", help="only the write-through-shaped chunk sizes")
     args = ap.parse_args()
     args.engines = [int(x) for x in args.engines.split(",")]
+    if args.wt_only:
+        pool = KvPool(64, 64, 32, 8, 128, device=torch.device("cuda"))
+        rows = wt_chunks(pool, args)
+        Path(args.out).parent.mkdir(parents=True, exist_ok=True)
+        Path(args.out).write_text(json.dumps({"wt_chunks": rows}, indent=1))
+        return
     sweep(args)
 
 

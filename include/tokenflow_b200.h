@@ -101,6 +101,12 @@ int tf_kv_scatter_h2d(int64_t pool, const tf_seg* segs, int32_t n_segs, int32_t 
  * transfers queued on the copy engines.  bytes <= 64 MiB. */
 int tf_copy_small(void* dst, const void* src, int64_t bytes, void* stream);
 
+/* Fused decode-forward ops between the library GEMMs (bf16 in / out, fp32
+ * math): y = x * rsqrt(mean(x^2) + eps) * w per row (dim % 8 == 0, dim <=
+ * 8192), and y = silu(gu[:, :ffn]) * gu[:, ffn:] for gu [rows][2*ffn]. */
+int tf_rmsnorm(const void* x, const void* w, void* y, int32_t rows, int32_t dim, float eps, void* stream);
+int tf_silu_mul(const void* gu, void* y, int32_t rows, int32_t ffn, void* stream);
+
 /* ---------------------------------------------------------------- KV append --
  * Model path: write K/V rows of n tokens for one layer, token i at
  * (table[rows[i]], pos[i]).  k/v: [n][kv_heads][head_dim] bf16 with a row

@@ -1137,7 +1137,7 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
   if (waves < 0) {
     const char* w = getenv("TF_ATTN_WAVES");
     const char* m = getenv("TF_ATTN_MINBLK");
-    waves = w ? std::max(1, atoi(w)) : 4;
+    waves = w ? std::max(1, atoi(w)) : 2;  // tuned: profiles/r1_attn_plan_tuning.json
     minblk = m ? std::max(1, atoi(m)) : 8;
   }
   const int target = attn_impl() >= 2 ? 148 * 2 * waves : 148 * 6;  // v2/v3 run 2 CTAs per SM

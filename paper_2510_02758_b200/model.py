@@ -94,7 +94,12 @@ class PagedDecoder:
         return self.prompts[rid]
 
     def _rms(self, x, w):
-        return F.rms_norm(x, (x.shape[-1],), w, self.s.rms_eps)
+        x = x.contiguous()
+        y = torch.empty_like(x)
+        check(lib.tf_rmsnorm(C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr()),
+                             x.numel() // x.shape[-1], x.shape[-1], self.s.rms_eps,
+                             C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tf_rmsnorm")
+        return y
 
     def _rope(self, x, pos):
         # x [n, heads, hd], pos [n] (int64)
@@ -126,8 +131,10 @@ class PagedDecoder:
     def _mlp(self, x, L):
         h = self._rms(x, L["ln2"])
         gu = h @ L["wgu"]
-        g, u = gu.chunk(2, dim=-1)
-        return self._proj_residual(x, F.silu(g) * u, L["wd"])
+        act = torch.empty((gu.shape[0], self.ffn), device=gu.device, dtype=gu.dtype)
+        check(lib.tf_silu_mul(C.c_void_p(gu.data_ptr()), C.c_void_p(act.data_ptr()), gu.shape[0], self.ffn,
+                              C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tf_silu_mul")
+        return self._proj_residual(x, act, L["wd"])
 
     # ------------------------------------------------------------ forward passes
     @torch.no_grad()

@@ -196,3 +196,33 @@ def test_kv_append_writes_slots(cuda):
         assert torch.equal(g[blk, 1, 0, :, slot], kvc[i, 0])
         assert torch.equal(g[blk, 1, 1, :, slot], kvc[i, 1])
     p.close()
+
+
+@pytest.mark.parametrize("rows,dim", [(1, 256), (37, 4096), (128, 5120), (3000, 4096)])
+def test_rmsnorm_vs_torch(cuda, rows, dim):
+    import torch.nn.functional as F
+
+    lib = _lib()
+    x = (torch.randn(rows, dim, device=cuda) * 3).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(dim, device=cuda)).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    lib.check(lib.lib.tf_rmsnorm(C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr()),
+                                 rows, dim, 1e-5, None))
+    torch.cuda.synchronize()
+    ref = F.rms_norm(x.float(), (dim,), w.float(), 1e-5)
+    # bf16 output: within 2 bf16 ulps of the fp32 reference
+    assert ((y.float() - ref).abs() <= 2 ** -6 * ref.abs() + 1e-3).all()
+
+
+@pytest.mark.parametrize("rows,ffn", [(1, 688), (64, 14336), (200, 3456)])
+def test_silu_mul_vs_torch(cuda, rows, ffn):
+    import torch.nn.functional as F
+
+    lib = _lib()
+    gu = (torch.randn(rows, 2 * ffn, device=cuda) * 2).to(torch.bfloat16)
+    y = torch.empty(rows, ffn, device=cuda, dtype=torch.bfloat16)
+    lib.check(lib.lib.tf_silu_mul(C.c_void_p(gu.data_ptr()), C.c_void_p(y.data_ptr()), rows, ffn, None))
+    torch.cuda.synchronize()
+    g, u = gu.float().chunk(2, dim=-1)
+    ref = F.silu(g) * u
+    assert ((y.float() - ref).abs() <= 2 ** -6 * ref.abs() + 1e-3).all()
