@@ -194,6 +194,7 @@ def run_ours(args):
         orig_tick = policy.on_tick
 
         def on_tick(view):
+            tp_before, mode_before = dict(policy._t_prime), policy.mode
             dec = orig_tick(view)
             if lo_t <= view.now <= hi_t:
                 snap = {k: getattr(view, k) for k in ("now", "free_slots", "gpu_mem_free", "gpu_mem_total",
@@ -201,7 +202,9 @@ def run_ours(args):
                                                       "offload_enabled", "h2d_blocked_tokens")}
                 snap["members"] = [dataclasses.asdict(m) for m in view.members]
                 snap["waiting"] = [dataclasses.asdict(w) for w in view.waiting]
-                tick_dump.append({"snapshot": snap, "mode": dec.mode, "preempt": list(dec.preempt),
+                tick_dump.append({"snapshot": snap, "t_prime": sorted(tp_before.items()), "mode_before": mode_before,
+                                  "t_prime_after": sorted(policy._t_prime.items()),
+                                  "mode": dec.mode, "preempt": list(dec.preempt),
                                   "resume": [list(r) for r in dec.resume],
                                   "prefill_batches": [list(b) for b in dec.prefill_batches]})
             return dec
