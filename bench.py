@@ -182,6 +182,10 @@ def run_ours(args):
                       n_q_heads=shape.n_q_heads // tp_size, engine=args.swap_engine)
     if args.fused_wt:
         dp.enable_fused_write_through()
+    if args.profile_hooks:
+        from paper_2510_02758_b200.dataplane import profile_hooks
+
+        profile_hooks(dp)
     if args.graphs:
         dp.enable_scratch()
         model.enable_graphs(dp)
@@ -216,6 +220,45 @@ def run_ours(args):
     t_start = time.perf_counter()
     state = {"phase": "warm", "timed": [], "wall0": None, "wall1": None}
 
+    def window_probes(eng, timed):
+        """Right at the end of the timed window (device idle, live batch intact):
+        the roofline of the dominant kernel (paged attention re-launched on the
+        largest timed batch's still-resident members, all layers, CUDA events)
+        and transfer hidden under the captured decode of that batch."""
+        torch.cuda.synchronize()
+        hbm, peak_kind = _peaks()
+        big = max(timed, key=lambda r: r["batch"])
+        live = [r for r in big["rids"] if eng.state[r].status == "running"]
+        if not live:
+            return
+        per = model.measure_attention(dp, live, [eng.state[r].kv.total_kv - 1 for r in live])
+        avg_ms = sum(ms for _, ms in per) / len(per)
+        avg_bytes = sum(b for b, _ in per) / len(per)
+        ach = avg_bytes / (avg_ms / 1e3) / 1e9
+        G = shape.n_q_heads // shape.n_kv_heads
+        kname = {"1": "paged_attn_kernel (v1)", "2": "paged_attn_tma_kernel (v2)",
+                 "3": f"paged_attn_mma_kernel<{G}> (v3) + combine"}.get(
+            os.environ.get("TF_ATTN_IMPL", "3")[:1], f"paged_attn_stream_kernel<{G}> (v4 stream-K, tensor cores)")
+        traffic, tsrc = _ncu_traffic(avg_bytes)
+        state["roof"] = {"bound": "hbm", "kernel": kname, "achieved": round(ach, 1),
+                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                         "traffic": traffic, "traffic_source": tsrc,
+                         "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live),
+                         "algorithmic_bytes_per_launch": round(avg_bytes),
+                         "note": f"bytes = sum(ctx) x {pool.H * pool.D * 4} B (K+V, {pool.H} kv heads x {pool.D} x "
+                                 "bf16) + q/out + table entries per layer; re-launched on the window's largest "
+                                 "batch right after the window"}
+        if args.graphs:
+            xf = dp.transfer_log()[state["ev0"]:state["ev1"]]
+            per_step = lambda k: math.ceil(sum(n for d, n, _ in xf if d == k) / 16 / len(timed))  # noqa: E731
+            hid_w = measure_hidden(model, dp, eng, live, per_step("d2h"), per_step("h2d"))
+            # blocks per direction that keep a ~55 GB/s link busy for one decode step
+            sat = max(1, int(55e9 * (hid_w["t_decode_ms"] if hid_w else 7.0) / 1e3 / dp.pool.block_bytes))
+            hid_s = measure_hidden(model, dp, eng, live, sat, sat)
+            state["hidden"] = {"window_volume": hid_w, "link_saturating": hid_s,
+                               "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = the captured forward of "
+                                       "the live batch; swaps on copy engines, own streams"}
+
     def on_step(rec, eng):
         n = len(eng.steps)
         if args.verbose and n % 100 == 0:
@@ -239,8 +282,18 @@ def run_ours(args):
                 state["pre1"], state["rc1"] = eng.total_preemptions, eng.total_recomputes
                 state["phase"] = "done"
                 torch.cuda.nvtx.range_pop()
-                if not args.full_run:
+                t_p = time.perf_counter()
+                window_probes(eng, state["timed"])
+                if args.full_run or args.ttft:
+                    # the probes' pause is not serving time: shift the real-time clock back
+                    eng.shift_clock(time.perf_counter() - t_p)
+                    state["phase"] = "ttft" if not args.full_run else "rest"
+                else:
                     eng._stop = True
+            return
+        if state["phase"] == "ttft" and all(st.record.gen_times for st in eng.state.values()):
+            state["ttft_done_at"] = eng.now
+            eng._stop = True
 
     eng = RealtimeEngine(tr, policy, cm, sim, dp, skip_idle=True, on_step=on_step, lockstep=lockstep,
                          max_wall_s=args.max_wall if args.full_run else None)
@@ -255,7 +308,7 @@ def run_ours(args):
     with sampler:
         res = eng.run()
     torch.cuda.synchronize()
-    if state["phase"] != "done":
+    if state["phase"] not in ("done", "ttft", "rest"):
         raise RuntimeError(f"bench ended in phase {state['phase']} after {len(eng.steps)} steps")
     timed = state["timed"]
     # device time of the window: every GPU job (decode iterations and the
@@ -289,42 +342,9 @@ def run_ours(args):
     for k in ("d2h", "h2d"):
         if swap[f"{k}_gbs"]:
             swap[f"{k}_frac_pcie"] = swap[f"{k}_gbs"] / PCIE_GEN5_GBS
-    # roofline of the dominant hand-written kernel (paged decode attention),
-    # timed with CUDA events on the live pool: the largest timed batch's
-    # members that are still resident, all 32 layers
-    hbm, peak_kind = _peaks()
-    roof = None
-    big = max(timed, key=lambda r: r["batch"])
-    # (a --full-run has served the whole trace by now: no live batch left to probe)
-    live = [] if args.full_run else [r for r in big["rids"] if eng.state[r].status == "running"]
-    if live:
-        per = model.measure_attention(dp, live, [eng.state[r].kv.total_kv - 1 for r in live])
-        avg_ms = sum(ms for _, ms in per) / len(per)
-        avg_bytes = sum(b for b, _ in per) / len(per)
-        ach = avg_bytes / (avg_ms / 1e3) / 1e9
-        G = shape.n_q_heads // shape.n_kv_heads
-        kname = {"1": "paged_attn_kernel (v1)", "2": "paged_attn_tma_kernel (v2)",
-                 "3": f"paged_attn_mma_kernel<{G}> (v3) + combine"}.get(
-            os.environ.get("TF_ATTN_IMPL", "3")[:1], f"paged_attn_stream_kernel<{G}> (v4 stream-K, tensor cores)")
-        traffic, tsrc = _ncu_traffic(avg_bytes)
-        roof = {"bound": "hbm", "kernel": kname, "achieved": round(ach, 1),
-                "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4),
-                "traffic": traffic, "traffic_source": tsrc,
-                "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live),
-                "algorithmic_bytes_per_launch": round(avg_bytes),
-                "note": f"bytes = sum(ctx) x {pool.H * pool.D * 4} B (K+V, {pool.H} kv heads x {pool.D} x bf16) + "
-                        "q/out + table entries per layer"}
-    # transfer hidden under decode, at the window's own swap volume per step
-    # and at a link-saturating volume (swap time ~= decode time)
-    if live and args.graphs:
-        per_step = lambda n: math.ceil(n / 16 / len(timed))  # noqa: E731
-        hid_w = measure_hidden(model, dp, eng, live, per_step(d2h_tok), per_step(h2d_tok))
-        # blocks per direction that keep a ~55 GB/s link busy for one decode step
-        sat = max(1, int(55e9 * (hid_w["t_decode_ms"] if hid_w else 7.0) / 1e3 / dp.pool.block_bytes))
-        hid_s = measure_hidden(model, dp, eng, live, sat, sat)
-        swap["hidden_under_decode"] = {"window_volume": hid_w, "link_saturating": hid_s,
-                                       "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = the captured "
-                                               "forward of the live batch; swaps on copy engines, own streams"}
+    roof = state.get("roof")
+    if state.get("hidden"):
+        swap["hidden_under_decode"] = state["hidden"]
     ttft = [r for r in res.records if r.gen_times]
     out = {
         "metric": METRIC,
@@ -365,6 +385,12 @@ def run_ours(args):
         "clocks": sampler.summary(),
         "gpu_launches": None,
         "first_tokens_in_window": len(ttft),
+        "ttft": ({"p99_s": round(ttft_latency_stats(ttft)["p99"], 4), "p50_s": round(ttft_latency_stats(ttft)["p50"], 4),
+                  "mean_s": round(ttft_latency_stats(ttft)["mean"], 4), "requests": len(ttft),
+                  "of": len(res.records), "complete": len(ttft) == len(res.records),
+                  "note": "TTFT latency = first token - arrival (nearest-rank P99, tokensim/metrics.py:144-155), "
+                          "real-time serving continued after the window until every request had its first token"}
+                 if ttft else None),
     }
     # this package's kernels per decode step: fused rope/append(+write-through) and
     # paged attention per layer, the zero-copy step input / sampled-id copies;
@@ -383,6 +409,9 @@ def run_ours(args):
         if not eng.truncated:
             out["full_run"]["effective_tok_s"] = effective_throughput(res.records, res.total_time,
                                                                       EffectiveThroughputConfig())
+    if args.profile_hooks:
+        out["host_hook_ms"] = {k: {"calls": c, "avg_ms": round(t / c * 1e3, 4), "total_s": round(t, 3)}
+                               for k, (c, t) in dp.hook_time.items() if c}
     if args.dump_ticks:
         import gzip
 
@@ -549,6 +578,8 @@ def main():
                     "makes every preemption an instant full release, which tips the reference policy into "
                     "preempt/recompute churn on the C2 burst (DESIGN.md section 7)")
     ap.add_argument("--full-run", action="store_true")
+    ap.add_argument("--ttft", type=int, default=1, help="after the window keep serving until every request has "
+                    "its first token (complete P99 TTFT of the burst)")
     ap.add_argument("--max-wall", type=float, default=600.0, help="--full-run: stop (truncated) after this many "
                     "seconds of wall time")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
@@ -556,6 +587,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--watchdog", type=float, default=0.0, help="debug: dump engine state every N seconds")
+    ap.add_argument("--profile-hooks", action="store_true", help="debug: host time per data-plane hook")
     ap.add_argument("--dump-ticks", default=None, help="debug: gzip JSON of the policy's snapshots + decisions")
     ap.add_argument("--dump-window", default="0,1e9", help="debug: virtual-time window of --dump-ticks")
     args = ap.parse_args()

@@ -144,6 +144,7 @@ class GpuDataPlane:
         self._d2h_busy = None  # (rid, lo, hi, kind, event)
         self._last_d2h_event = {}  # rid -> event of its last d2h (loads of that range wait on it)
         self._quarantine: deque = deque()  # (event, [blocks]) realtime frees awaiting their fence
+        self._q_blocks = 0  # blocks held in the quarantine
         self.peak_blocks = 0
         self.peak_host_blocks = 0
         self.stats = {"d2h_tokens": 0, "h2d_tokens": 0, "d2h_launches": 0, "h2d_launches": 0, "append_tokens": 0,
@@ -189,7 +190,7 @@ class GpuDataPlane:
             for j, b in zip(need, ids):
                 tab[j] = b
                 self._pending_table.append((rid, j, b))
-        used = self.pool.n_blocks - self.pool.free_count(TIER_GPU) - sum(len(b) for _, b in self._quarantine)
+        used = self.pool.n_blocks - self.pool.free_count(TIER_GPU) - self._q_blocks
         self.peak_blocks = max(self.peak_blocks, used)
 
     def _release_blocks(self, ids):
@@ -203,13 +204,17 @@ class GpuDataPlane:
                 ev.record(s)
                 evs.append(ev)
             self._quarantine.append((evs, ids))
+            self._q_blocks += len(ids)
 
     def _alloc_blocks(self, n):
         if self.mode == "realtime":
             while self._quarantine and all(e.query() for e in self._quarantine[0][0]):
-                self.pool.free(TIER_GPU, self._quarantine.popleft()[1])
+                ids = self._quarantine.popleft()[1]
+                self._q_blocks -= len(ids)
+                self.pool.free(TIER_GPU, ids)
             while self._quarantine and self.pool.free_count(TIER_GPU) < n:
                 evs, ids = self._quarantine.popleft()
+                self._q_blocks -= len(ids)
                 for e in evs:
                     e.synchronize()
                 self.pool.free(TIER_GPU, ids)
@@ -577,3 +582,27 @@ class GpuDataPlane:
         """(direction, tokens, ms) of every launched chunk (synchronises)."""
         self.synchronize()
         return [(k, n, a.elapsed_time(b)) for k, n, a, b in self._events]
+
+
+def profile_hooks(dp):
+    """Debug aid: accumulate the host wall time of every engine hook of ``dp``
+    (dp.hook_time[name] = [calls, seconds])."""
+    import functools
+    import time as _time
+
+    dp.hook_time = {}
+    for name in ("fill_start", "fill_done", "decode_start", "decode_done", "d2h_start", "d2h_done", "h2d_start",
+                 "release_prefix", "drop_gpu", "drop_host", "finish"):
+        fn = getattr(dp, name)
+
+        def wrap(*a, _fn=fn, _name=name, **k):
+            t = _time.perf_counter()
+            try:
+                return _fn(*a, **k)
+            finally:
+                rec = dp.hook_time.setdefault(_name, [0, 0.0])
+                rec[0] += 1
+                rec[1] += _time.perf_counter() - t
+
+        setattr(dp, name, functools.wraps(fn)(wrap))
+    return dp

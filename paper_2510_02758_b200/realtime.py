@@ -82,6 +82,12 @@ class RealtimeEngine(Engine):
     def _clock(self) -> float:
         return time.perf_counter() - self._t0 + self.skipped_s
 
+    def shift_clock(self, dt: float):
+        """Exclude ``dt`` seconds of wall time (e.g. a measurement pause) from the
+        serving clock."""
+        self._t0 += dt
+        self._reanchor()
+
     def _reanchor(self):
         ev = self.dp.record_event()
         ev.synchronize()

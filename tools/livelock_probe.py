@@ -28,25 +28,39 @@ from paper_2510_02758_b200.scheduler import BufferAwarePolicy, SchedulerConfig  
 from paper_2510_02758_b200.workload import load_trace  # noqa: E402
 
 
+def _spin(ms):
+    if ms > 0:
+        t = time.perf_counter() + ms / 1e3
+        while time.perf_counter() < t:
+            pass
+
+
 class B200Plane(TimedPlane):
-    def __init__(self, fused):
+    def __init__(self, fused, host_ms=(0.0, 0.0, 0.0)):
         super().__init__(0, 0.0)
         self.fused_wt = fused
+        self.host_decode, self.host_copy, self.host_fill = host_ms
 
     def host_frontier(self, rid, cs, total):
         return total
 
     def fill_start(self, job, eng):
         self._run("c", 1e-3 + 1.76e-5 * job.process_tokens)
+        _spin(self.host_fill)
 
     def decode_start(self, batch, eng):
         self._run("c", 1.5e-3 + 1.5e-5 * len(batch) + 1.2e-8 * sum(eng.state[r].kv.total_kv for r in batch))
+        _spin(self.host_decode)
 
     def d2h_start(self, ch, eng):
-        return self._run("d2h", 1e-5 + ch.tokens / 420000)
+        ev = self._run("d2h", 1e-5 + ch.tokens / 420000)
+        _spin(self.host_copy)
+        return ev
 
     def h2d_start(self, ch, eng):
-        return self._run("h2d", 1e-5 + ch.tokens / 420000)
+        ev = self._run("h2d", 1e-5 + ch.tokens / 420000)
+        _spin(self.host_copy)
+        return ev
 
 
 def main():
@@ -55,6 +69,7 @@ def main():
     ap.add_argument("--fused", type=int, default=0)
     ap.add_argument("--max-wall", type=float, default=300)
     ap.add_argument("--arrivals", default="burst")
+    ap.add_argument("--host-ms", default="0,0,0", help="host time spent per decode / copy / prefill launch (ms)")
     args = ap.parse_args()
     c2 = configs.C2
     name = "c2_burst256_s1" if args.arrivals == "burst" else "c2_poisson256_s1"
@@ -67,7 +82,7 @@ def main():
 
         pol = build_policy("tokenflow", Knobs(**asdict(scfg)))
     eng = RealtimeEngine(tr, pol, c2.cost_model(CostModel), c2.sim_cfg(SimConfig, debug_checks=False),
-                         B200Plane(bool(args.fused)), skip_idle=True, max_wall_s=args.max_wall)
+                         B200Plane(bool(args.fused), tuple(float(x) for x in args.host_ms.split(","))), skip_idle=True, max_wall_s=args.max_wall)
     t0 = time.time()
     res = eng.run()
     st = collections.Counter(s.status for s in eng.state.values())
