@@ -592,7 +592,8 @@ def main():
     ap.add_argument("--dump-window", default="0,1e9", help="debug: virtual-time window of --dump-ticks")
     args = ap.parse_args()
     if args.host_blocks <= 0:
-        args.host_blocks = 26000 if args.full_run else 16384
+        # a full run / the TTFT continuation of the burst peaks near 22K blocks
+        args.host_blocks = 26000 if (args.full_run or args.ttft) else 16384
         # never pin more than ~60% of the host's available RAM across the
         # node's ranks (one pinned host tier per GPU replica)
         try:

@@ -20,8 +20,7 @@ import ctypes as C
 import math
 
 import torch
-import torch.nn.functional as F
-from torch.nn.attention import SDPBackend, sdpa_kernel
+from torch.nn.attention.varlen import varlen_attn
 
 from . import _lib
 from ._lib import check, lib
@@ -145,11 +144,18 @@ class PagedDecoder:
         Returns the argmax token after each sequence's last position (device)."""
         s = self.s
         lens = [t.numel() for _, t, _ in seqs]
+        # every host->device input goes through pinned memory, non-blocking: a
+        # pageable copy would block the host until the compute stream drains
         toks = torch.cat([t for _, t, _ in seqs]).pin_memory().to(self.device, non_blocking=True)
-        meta = torch.tensor([[rid, p0 + i] for rid, t, p0 in seqs for i in range(t.numel())],
-                            dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
-        rows, pos32 = meta[:, 0].contiguous(), meta[:, 1].contiguous()
+        rows_h = torch.repeat_interleave(torch.tensor([rid for rid, _, _ in seqs], dtype=torch.int32),
+                                         torch.tensor(lens))
+        pos_h = torch.cat([torch.arange(p0, p0 + t.numel(), dtype=torch.int32) for _, t, p0 in seqs])
+        cu_h = torch.zeros(len(lens) + 1, dtype=torch.int32)
+        cu_h[1:] = torch.cumsum(torch.tensor(lens, dtype=torch.int32), 0)
+        meta = torch.cat([rows_h, pos_h, cu_h]).pin_memory().to(self.device, non_blocking=True)
         n = toks.numel()
+        rows, pos32, cu = meta[:n], meta[n:2 * n], meta[2 * n:]
+        max_len = max(lens)
         G = self.hq // self.hkv
         x = self.embed[toks]
         q = torch.empty((n, self.hq, s.head_dim), device=self.device, dtype=x.dtype)
@@ -174,18 +180,15 @@ class PagedDecoder:
                                             C.c_void_p(self._inv_freq.data_ptr()), C.c_void_p(q.data_ptr()),
                                             C.c_void_p(kvb.data_ptr()), C.c_void_p(st.cuda_stream)),
                       "tf_rope_kv_append")
-            outs, o = [], 0
-            with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION]):
-                for ln in lens:
-                    qi = q[o:o + ln].transpose(0, 1)[None]
-                    ki = k[o:o + ln].repeat_interleave(G, dim=1).transpose(0, 1)[None]
-                    vi = v[o:o + ln].repeat_interleave(G, dim=1).transpose(0, 1)[None]
-                    outs.append(F.scaled_dot_product_attention(qi, ki, vi, is_causal=True)[0].transpose(0, 1))
-                    o += ln
-            a = torch.cat(outs).reshape(n, -1)
+            # causal attention over every sequence of the batch in ONE varlen
+            # flash-attention call (library kernel; per-sequence launches made
+            # the host the bottleneck of recompute-heavy phases)
+            kx = k.repeat_interleave(G, dim=1) if G > 1 else k
+            vx = v.repeat_interleave(G, dim=1) if G > 1 else v
+            a = varlen_attn(q, kx, vx, cu, cu, max_len, max_len, window_size=(-1, 0)).reshape(n, -1)
             x = self._proj_residual(x, a, L["wo"])
             x = self._mlp(x, L)
-        last = torch.tensor(list(_cumsum(lens)), device=self.device) - 1
+        last = (cu[1:] - 1).long()
         return (self._rms(x[last], self.ln_f) @ self.lm_head).argmax(-1)
 
     @torch.no_grad()
@@ -397,10 +400,3 @@ class PagedDecoder:
             x = self._proj_residual(x, attn.view(B, -1), L["wo"])
             x = self._mlp(x, L)
         return (self._rms(x, self.ln_f) @ self.lm_head).argmax(-1)
-
-
-def _cumsum(xs):
-    acc = 0
-    for x in xs:
-        acc += x
-        yield acc
