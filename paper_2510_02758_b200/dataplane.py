@@ -173,23 +173,23 @@ class GpuDataPlane:
     # ------------------------------------------------------------ block table
     def _reconcile(self, rid, blocks):
         f, tab = self.flags[rid], self.gtab[rid]
-        blocks = sorted(set(int(j) for j in blocks))
-        # HBM occupancy = LIVE | DETACHED | RESERVED (HOSTV only marks the host mirror)
-        occ = [bool((f[j * self.B:(j + 1) * self.B] & 7).any()) for j in blocks]
-        freed = []
-        for j, o in zip(blocks, occ):
-            if not o and tab[j] >= 0:
-                freed.append(int(tab[j]))
-                tab[j] = -1
-                self._pending_table.append((rid, j, -1))
-        if freed:
-            self._release_blocks(freed)
-        need = [j for j, o in zip(blocks, occ) if o and tab[j] < 0]
-        if need:
-            ids = self._alloc_blocks(len(need))
-            for j, b in zip(need, ids):
-                tab[j] = b
-                self._pending_table.append((rid, j, b))
+        blocks = np.unique(np.fromiter(blocks, dtype=np.int64) if not isinstance(blocks, np.ndarray)
+                           else blocks.astype(np.int64, copy=False))
+        if blocks.size:
+            # HBM occupancy = LIVE | DETACHED | RESERVED (HOSTV only marks the host mirror)
+            occ = (f.reshape(-1, self.B)[blocks] & 7).any(axis=1)
+            mapped = tab[blocks] >= 0
+            fr = blocks[~occ & mapped]  # ascending: frees first (LIFO push) ...
+            if fr.size:
+                freed = tab[fr].tolist()
+                tab[fr] = -1
+                self._pending_table.extend((rid, j, -1) for j in fr.tolist())
+                self._release_blocks(freed)
+            need = blocks[occ & ~mapped]  # ... then allocations (pop), ascending
+            if need.size:
+                ids = self._alloc_blocks(len(need))
+                tab[need] = ids
+                self._pending_table.extend(zip([rid] * len(ids), need.tolist(), ids))
         used = self.pool.n_blocks - self.pool.free_count(TIER_GPU) - self._q_blocks
         self.peak_blocks = max(self.peak_blocks, used)
 
@@ -408,7 +408,7 @@ class GpuDataPlane:
         if len(miss) != ch.tokens or (len(miss) and miss[-1] >= self.host_hi[rid]):
             raise _lib.InvariantError(f"load of {rid} needs positions missing from the host store")
         f[miss] |= LIVE
-        self._reconcile(rid, {int(p) // self.B for p in miss})
+        self._reconcile(rid, miss // self.B)
         st = self.s_load
         ev = self._last_d2h_event.get(rid)
         if self.mode == "realtime" and ev is not None:
@@ -456,7 +456,7 @@ class GpuDataPlane:
         if len(idx) != n:
             raise _lib.InvariantError(f"instant release of {n} tokens but {len(idx)} resident")
         f[idx] &= CLR_LIVE
-        self._reconcile(rid, {int(i) // self.B for i in idx})
+        self._reconcile(rid, idx // self.B)
 
     def cancel_evicts(self, rid):
         pass
@@ -465,7 +465,7 @@ class GpuDataPlane:
         f = self.flags[rid]
         idx = np.nonzero(f & LIVE)[0]
         f[idx] &= CLR_LIVE
-        self._reconcile(rid, {int(i) // self.B for i in idx})
+        self._reconcile(rid, idx // self.B)
 
     def drop_host(self, rid):
         tab = self.htab[rid]
@@ -501,7 +501,7 @@ class GpuDataPlane:
         f = self.flags[rid]
         idx = np.nonzero(f)[0]
         f[:] = 0
-        self._reconcile(rid, {int(i) // self.B for i in idx})
+        self._reconcile(rid, idx // self.B)
         self.drop_host(rid)
 
     def audit(self, eng):
