@@ -34,12 +34,16 @@ Pool* get_pool(int64_t handle) {
 }
 
 // (row, lb, block) triples applied by one thread each.
+// Launch parameters sized to the delta: a typical decode step changes a few
+// table entries, and a 24 KB parameter block would dominate the launch cost.
+template <int CAP>
 struct TableOps {
   int32_t n;
-  int32_t v[3 * 2048];
+  int32_t v[3 * CAP];
 };
 
-__global__ void table_apply_kernel(int32_t* table, int32_t stride, const __grid_constant__ TableOps ops) {
+template <int CAP>
+__global__ void table_apply_kernel(int32_t* table, int32_t stride, const __grid_constant__ TableOps<CAP> ops) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < ops.n) {
     int32_t row = ops.v[3 * i], lb = ops.v[3 * i + 1], blk = ops.v[3 * i + 2];
@@ -152,10 +156,18 @@ int tf_table_apply(int32_t* dev_table, int32_t row_stride, const int32_t* triple
   TF_CHECK_ARG(dev_table && row_stride > 0, "tf_table_apply: bad table");
   TF_CHECK_ARG(n_triples >= 0 && (n_triples == 0 || triples), "tf_table_apply: bad triples");
   for (int32_t base = 0; base < n_triples; base += 2048) {
-    TableOps ops;
-    ops.n = n_triples - base < 2048 ? n_triples - base : 2048;
-    memcpy(ops.v, triples + 3 * base, sizeof(int32_t) * 3 * ops.n);
-    table_apply_kernel<<<(ops.n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(dev_table, row_stride, ops);
+    const int32_t n = n_triples - base < 2048 ? n_triples - base : 2048;
+    if (n <= 64) {
+      TableOps<64> ops;
+      ops.n = n;
+      memcpy(ops.v, triples + 3 * base, sizeof(int32_t) * 3 * n);
+      table_apply_kernel<64><<<1, 128, 0, (cudaStream_t)stream>>>(dev_table, row_stride, ops);
+    } else {
+      TableOps<2048> ops;
+      ops.n = n;
+      memcpy(ops.v, triples + 3 * base, sizeof(int32_t) * 3 * n);
+      table_apply_kernel<2048><<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(dev_table, row_stride, ops);
+    }
     TF_LAUNCH_CHECK();
   }
   return TF_OK;

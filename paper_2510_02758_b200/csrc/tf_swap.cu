@@ -25,13 +25,17 @@ constexpr int kMaxSegs = 1536;
 constexpr int kSwapThreads = 256;
 constexpr int kUnroll = 8;
 
+// Segment capacity is a template parameter so a small chunk (write-through
+// tails: 1-3 segments) launches with a few hundred bytes of parameters
+// instead of 18 KB.
+template <int CAP>
 struct SwapArgs {
   PoolView pv;
   int32_t layer_begin, layer_end, n_segs, to_host;
-  int32_t gpu_block[kMaxSegs];
-  int32_t host_block[kMaxSegs];
-  int16_t slot_begin[kMaxSegs];
-  int16_t n_slots[kMaxSegs];
+  int32_t gpu_block[CAP];
+  int32_t host_block[CAP];
+  int16_t slot_begin[CAP];
+  int16_t n_slots[CAP];
 };
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
@@ -55,7 +59,8 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
 
 // blockIdx.y = segment; the segment's vectors (16 B) are enumerated as
 // run-major (layer, kv, head) x (slot, dim/8) and strided over blockIdx.x.
-__global__ void __launch_bounds__(kSwapThreads) swap_kernel(const __grid_constant__ SwapArgs a) {
+template <int CAP>
+__global__ void __launch_bounds__(kSwapThreads) swap_kernel(const __grid_constant__ SwapArgs<CAP> a) {
   const int s = blockIdx.y;
   const PoolView& pv = a.pv;
   const int ns = a.n_slots[s];
@@ -97,33 +102,41 @@ __global__ void __launch_bounds__(kSwapThreads) swap_kernel(const __grid_constan
   }
 }
 
+template <int CAP>
+static int swap_sm_launch(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int to_host,
+                          cudaStream_t st) {
+  SwapArgs<CAP> a;
+  a.pv = view_of(p);
+  a.layer_begin = l0;
+  a.layer_end = l1;
+  a.to_host = to_host;
+  a.n_segs = n;
+  int64_t max_vec = 0;
+  for (int i = 0; i < n; ++i) {
+    const tf_seg& s = segs[i];
+    a.gpu_block[i] = s.gpu_block;
+    a.host_block[i] = s.host_block;
+    a.slot_begin[i] = (int16_t)s.slot_begin;
+    a.n_slots[i] = (int16_t)s.n_slots;
+    max_vec = std::max(max_vec, (int64_t)(l1 - l0) * 2 * p.kv_heads * s.n_slots * p.head_dim / 8);
+  }
+  // PCIe-bound: ~128 CTAs of 256 threads x 8 x 16 B keep > 4 MB in flight.
+  int64_t want = (max_vec + (int64_t)kSwapThreads * kUnroll - 1) / ((int64_t)kSwapThreads * kUnroll);
+  int64_t cap = std::max<int64_t>(1, 128 / std::max<int32_t>(1, n));
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, cap)), (unsigned)n);
+  swap_kernel<CAP><<<grid, kSwapThreads, 0, st>>>(a);
+  TF_LAUNCH_CHECK();
+  return TF_OK;
+}
+
 static int swap_sm(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int to_host,
                    cudaStream_t st) {
   for (int32_t base = 0; base < n; base += kMaxSegs) {
-    SwapArgs a;
-    a.pv = view_of(p);
-    a.layer_begin = l0;
-    a.layer_end = l1;
-    a.to_host = to_host;
-    a.n_segs = std::min<int32_t>(kMaxSegs, n - base);
-    int64_t max_vec = 0, tot_vec = 0;
-    for (int i = 0; i < a.n_segs; ++i) {
-      const tf_seg& s = segs[base + i];
-      a.gpu_block[i] = s.gpu_block;
-      a.host_block[i] = s.host_block;
-      a.slot_begin[i] = (int16_t)s.slot_begin;
-      a.n_slots[i] = (int16_t)s.n_slots;
-      int64_t v = (int64_t)(l1 - l0) * 2 * p.kv_heads * s.n_slots * p.head_dim / 8;
-      max_vec = std::max(max_vec, v);
-      tot_vec += v;
-    }
-    // PCIe-bound: ~128 CTAs of 256 threads x 8 x 16 B keep > 4 MB in flight.
-    int64_t want = (max_vec + (int64_t)kSwapThreads * kUnroll - 1) / ((int64_t)kSwapThreads * kUnroll);
-    int64_t cap = std::max<int64_t>(1, 128 / std::max<int32_t>(1, a.n_segs));
-    dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, cap)), (unsigned)a.n_segs);
-    swap_kernel<<<grid, kSwapThreads, 0, st>>>(a);
-    TF_LAUNCH_CHECK();
-    (void)tot_vec;
+    const int32_t m = std::min<int32_t>(kMaxSegs, n - base);
+    int rc = m <= 8 ? swap_sm_launch<8>(p, segs + base, m, l0, l1, to_host, st)
+             : m <= 64 ? swap_sm_launch<64>(p, segs + base, m, l0, l1, to_host, st)
+                       : swap_sm_launch<kMaxSegs>(p, segs + base, m, l0, l1, to_host, st);
+    if (rc != TF_OK) return rc;
   }
   return TF_OK;
 }
