@@ -578,8 +578,8 @@ def main():
                     "makes every preemption an instant full release, which tips the reference policy into "
                     "preempt/recompute churn on the C2 burst (DESIGN.md section 7)")
     ap.add_argument("--full-run", action="store_true")
-    ap.add_argument("--ttft", type=int, default=1, help="after the window keep serving until every request has "
-                    "its first token (complete P99 TTFT of the burst)")
+    ap.add_argument("--ttft", type=int, default=-1, help="after the window keep serving until every request has "
+                    "its first token (complete P99 TTFT of the burst); default on for c2, off for c4")
     ap.add_argument("--max-wall", type=float, default=600.0, help="--full-run: stop (truncated) after this many "
                     "seconds of wall time")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
@@ -591,6 +591,8 @@ def main():
     ap.add_argument("--dump-ticks", default=None, help="debug: gzip JSON of the policy's snapshots + decisions")
     ap.add_argument("--dump-window", default="0,1e9", help="debug: virtual-time window of --dump-ticks")
     args = ap.parse_args()
+    if args.ttft < 0:
+        args.ttft = 1 if args.config == "c2" else 0
     if args.host_blocks <= 0:
         # a full run / the TTFT continuation of the burst peaks near 22K blocks
         args.host_blocks = 26000 if (args.full_run or args.ttft) else 16384
