@@ -392,12 +392,13 @@ def run_ours(args):
                           "real-time serving continued after the window until every request had its first token"}
                  if ttft else None),
     }
-    # this package's kernels per decode step: fused rope/append(+write-through) and
-    # paged attention per layer, the zero-copy step input / sampled-id copies;
-    # plus one swap launch per chunk (prefill jobs' kernels are not counted)
+    # this package's kernels per decode step: per layer the fused rope/append,
+    # paged attention (+ split combine for v3), two RMSNorms and the SwiGLU;
+    # the final RMSNorm; the zero-copy step input / sampled-id copies; plus one
+    # swap launch per chunk (prefill jobs' kernels are not counted)
     attn_per_layer = 2 if os.environ.get("TF_ATTN_IMPL", "3")[:1] in ("2", "3") else 1
-    out["gpu_launches"] = int(len(timed) * (shape.n_layers * (1 + attn_per_layer) + (2 if args.graphs else 0))
-                              + len(xfers))
+    per_step = shape.n_layers * (1 + attn_per_layer + 2 + 1) + 1 + (2 if args.graphs else 0)
+    out["gpu_launches"] = int(len(timed) * per_step + len(xfers))
     if args.full_run:
         from paper_2510_02758_b200.metrics import EffectiveThroughputConfig, effective_throughput
 

@@ -132,9 +132,9 @@ __global__ void copy_small_kernel(unsigned char* __restrict__ dst, const unsigne
                                   int64_t bytes) {
   const bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
   const int64_t nv = vec ? bytes / 16 : 0;
-  for (int64_t i = threadIdx.x; i < nv; i += blockDim.x)
-    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
-  for (int64_t i = nv * 16 + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < nv; i += nt) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (int64_t i = nv * 16 + tid; i < bytes; i += nt) dst[i] = src[i];
 }
 
 }  // namespace tf
@@ -147,7 +147,9 @@ int tf_copy_small(void* dst, const void* src, int64_t bytes, void* stream) {
   TF_CHECK_ARG(bytes >= 0 && bytes <= (64 << 20), "tf_copy_small: bytes %lld out of range", (long long)bytes);
   if (bytes == 0) return TF_OK;
   TF_CHECK_ARG(dst && src, "tf_copy_small: NULL pointer");
-  copy_small_kernel<<<1, 256, 0, (cudaStream_t)stream>>>((unsigned char*)dst, (const unsigned char*)src, bytes);
+  // one CTA for step-sized copies; up to 32 for prefill inputs (PCIe latency-bound)
+  const int grid = (int)std::min<int64_t>(32, std::max<int64_t>(1, bytes / (16 << 10)));
+  copy_small_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((unsigned char*)dst, (const unsigned char*)src, bytes);
   TF_LAUNCH_CHECK();
   return TF_OK;
 }

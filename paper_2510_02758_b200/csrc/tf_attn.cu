@@ -564,7 +564,6 @@ __global__ void __launch_bounds__((kConsumers + 1) * 32) paged_attn_tma_kernel(c
 // from the S accumulators as the A operand (no shuffle / smem round trip).
 // ~100 instructions per block per warp instead of ~1000 on the CUDA cores.
 constexpr int kV3Warps = 4;
-constexpr int kV3Stages = 3;
 constexpr int kRowPad = 136;  // bf16 elements per padded smem row (128 + 8)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -598,14 +597,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
          ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(hi)) << 16);
 }
 
-template <int G>
-__global__ void __launch_bounds__(kV3Warps * 32, 2) paged_attn_mma_kernel(const AttnArgs a) {
+// S = ring stages per warp (S - 1 blocks in flight); 2 stages fit 3 CTAs per
+// SM (12 warps), 3 stages 2 CTAs per SM (8 warps).
+template <int G, int S>
+__global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_kernel(const AttnArgs a) {
   constexpr int D = 128;
   static_assert(G >= 1 && G <= 8, "v3 packs the group into rows 0..7 of the 16-row tile");
+  static_assert(S >= 2 && S <= 4, "2..4 stages");
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // per warp: [kV3Stages][K|V][16 rows][kRowPad]
+  // per warp: [S][K|V][16 rows][kRowPad]
   constexpr int kTileElems = kBlk * kRowPad;
-  constexpr int kWarpElems = kV3Stages * 2 * kTileElems;
+  constexpr int kWarpElems = S * 2 * kTileElems;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw) + warp * kWarpElems;
 
@@ -623,11 +625,11 @@ __global__ void __launch_bounds__(kV3Warps * 32, 2) paged_attn_mma_kernel(const 
   const int64_t voff = (((int64_t)a.layer * 2 + 1) * a.kv_heads + kvh) * tile;
   const int32_t* trow = a.table + (int64_t)a.rows[b] * a.stride;
 
-  auto issue = [&](int j) {  // warp-local block j -> stage j % kV3Stages
+  auto issue = [&](int j) {  // warp-local block j -> stage j % S
     if (j < nmine) {
       const int blk = blk_lo + warp + j * kV3Warps;
       const int64_t base = (int64_t)__ldg(trow + blk) * a.block_elems;
-      uint16_t* ks = ring + (j % kV3Stages) * 2 * kTileElems;
+      uint16_t* ks = ring + (j % S) * 2 * kTileElems;
       uint16_t* vs = ks + kTileElems;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {  // 256 x 16 B per tile, 8 per lane
@@ -639,8 +641,8 @@ __global__ void __launch_bounds__(kV3Warps * 32, 2) paged_attn_mma_kernel(const 
     }
     cp_async_commit();
   };
-  issue(0);
-  issue(1);
+#pragma unroll
+  for (int p0 = 0; p0 < S - 1; ++p0) issue(p0);
 
   // Q as the A operand: rows 0..G-1 = the group's heads (scaled later), rest 0
   const int r0 = lane >> 2, cq = (lane & 3) * 2;
@@ -664,10 +666,10 @@ __global__ void __launch_bounds__(kV3Warps * 32, 2) paged_attn_mma_kernel(const 
   float m0 = -FLT_MAX, l0 = 0.f;  // row r0 (rows r0+8 are padding)
 
   for (int j = 0; j < nmine; ++j) {
-    issue(j + 2);
-    cp_async_wait<2>();
+    issue(j + S - 1);
+    cp_async_wait<S - 1>();
     __syncwarp();
-    const uint16_t* ks = ring + (j % kV3Stages) * 2 * kTileElems;
+    const uint16_t* ks = ring + (j % S) * 2 * kTileElems;
     const uint16_t* vs = ks + kTileElems;
     const int blk = blk_lo + warp + j * kV3Warps;
     // ---- S = Q K^T : two n-tiles of 8 tokens, 8 k-steps of 16 dims
@@ -1127,6 +1129,15 @@ static int attn_impl() {
   return impl;
 }
 
+static int v3_stages() {
+  static int st = -1;
+  if (st < 0) {
+    const char* e = getenv("TF_ATTN_STAGES");
+    st = (e && e[0] == '2') ? 2 : 3;
+  }
+  return st;
+}
+
 static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps) {
   const int nblk = std::max(1, (max_ctx + kBlk - 1) / kBlk);
   const int base = std::max(1, B * kv_heads);
@@ -1140,7 +1151,8 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
     waves = w ? std::max(1, atoi(w)) : 2;  // tuned: profiles/r1_attn_plan_tuning.json
     minblk = m ? std::max(1, atoi(m)) : 8;
   }
-  const int target = attn_impl() >= 2 ? 148 * 2 * waves : 148 * 6;  // v2/v3 run 2 CTAs per SM
+  const int per_sm = attn_impl() >= 3 ? (v3_stages() == 2 ? 3 : 2) : 2;  // resident CTAs per SM
+  const int target = attn_impl() >= 2 ? 148 * per_sm * waves : 148 * 6;
   int s = std::max(1, std::min((target + base - 1) / base, (nblk + minblk - 1) / minblk));
   int per = (nblk + s - 1) / s;
   s = (nblk + per - 1) / per;
@@ -1181,14 +1193,21 @@ static int launch(const AttnArgs& a, int B, cudaStream_t st) {
   }
   dim3 grid(a.splits, B * a.kv_heads);
   if (attn_impl() >= 3 && D == 128 && G <= 8) {
-    const int smem = kV3Warps * kV3Stages * 2 * kBlk * kRowPad * 2;
+    constexpr int GG = G <= 8 ? G : 8;
+    const int S = v3_stages();
+    const int smem = kV3Warps * S * 2 * kBlk * kRowPad * 2;
     static bool attr3 = false;
     if (!attr3) {
-      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<(G <= 8 ? G : 8)>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kV3Warps * 2 * 2 * kBlk * kRowPad * 2));
+      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kV3Warps * 3 * 2 * kBlk * kRowPad * 2));
       attr3 = true;
     }
-    paged_attn_mma_kernel<(G <= 8 ? G : 8)><<<grid, kV3Warps * 32, smem, st>>>(a);
+    if (S == 2)
+      paged_attn_mma_kernel<GG, 2><<<grid, kV3Warps * 32, smem, st>>>(a);
+    else
+      paged_attn_mma_kernel<GG, 3><<<grid, kV3Warps * 32, smem, st>>>(a);
   } else if (attn_impl() >= 2) {
     const int smem = kStages * 2 * kBlk * D * 2;
     static bool attr = false;

@@ -26,6 +26,30 @@ from . import _lib
 from ._lib import check, lib
 
 
+class _Staging:
+    """Grow-only pinned host + device buffer for a host -> device input:
+    one zero-copy transfer (tf_copy_small) on the compute stream, no pinned
+    allocation per call (cudaHostAlloc is slow) and no copy-engine queueing
+    behind KV loads.  Reused call after call: the engine runs one GPU job at a
+    time and the next call comes after the previous job completed."""
+
+    def __init__(self, device):
+        self.device = device
+        self.h = self.d = None
+
+    def to_device(self, t: torch.Tensor, stream) -> torch.Tensor:
+        t = t.contiguous()
+        nb = t.numel() * t.element_size()
+        if self.h is None or self.h.numel() < nb:
+            cap = max(nb, 2 * (self.h.numel() if self.h is not None else 0), 4096)
+            self.h = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+            self.d = torch.empty(cap, dtype=torch.uint8, device=self.device)
+        self.h[:nb].copy_(t.view(-1).view(torch.uint8))
+        check(lib.tf_copy_small(C.c_void_p(self.d.data_ptr()), C.c_void_p(self.h.data_ptr()), nb,
+                                C.c_void_p(stream.cuda_stream)), "tf_copy_small")
+        return self.d[:nb].view(t.dtype).view(t.shape)
+
+
 class PagedDecoder:
     def __init__(self, shape, device="cuda", seed=0, dtype=torch.bfloat16, max_batch=256, tp=None):
         """``tp`` (tp.TpGroup): keep this rank's 1/TP of the heads / MLP columns
@@ -83,6 +107,10 @@ class PagedDecoder:
         self._ws = torch.zeros(1, dtype=torch.uint8, device=self.device)
         self.steps = 0
         self.attn_timing = None  # list -> (algorithmic bytes, start event, end event) per attention launch
+        self._st_tok, self._st_meta, self._st_rows = (_Staging(self.device) for _ in range(3))
+        if self.device.type == "cuda":  # (a CPU-constructed model only serves weight-layout tests)
+            self._pf_out = torch.zeros(2 * 4096, dtype=torch.long, pin_memory=True)  # prefill t0 / t1 readback
+            self._dec_out = torch.zeros(4096, dtype=torch.long, pin_memory=True)  # sampled ids readback
         self._graphs = {}
 
     # ------------------------------------------------------------ pieces
@@ -146,13 +174,13 @@ class PagedDecoder:
         lens = [t.numel() for _, t, _ in seqs]
         # every host->device input goes through pinned memory, non-blocking: a
         # pageable copy would block the host until the compute stream drains
-        toks = torch.cat([t for _, t, _ in seqs]).pin_memory().to(self.device, non_blocking=True)
+        toks = self._st_tok.to_device(torch.cat([t for _, t, _ in seqs]), st)
         rows_h = torch.repeat_interleave(torch.tensor([rid for rid, _, _ in seqs], dtype=torch.int32),
                                          torch.tensor(lens))
         pos_h = torch.cat([torch.arange(p0, p0 + t.numel(), dtype=torch.int32) for _, t, p0 in seqs])
         cu_h = torch.zeros(len(lens) + 1, dtype=torch.int32)
         cu_h[1:] = torch.cumsum(torch.tensor(lens, dtype=torch.int32), 0)
-        meta = torch.cat([rows_h, pos_h, cu_h]).pin_memory().to(self.device, non_blocking=True)
+        meta = self._st_meta.to_device(torch.cat([rows_h, pos_h, cu_h]), st)
         n = toks.numel()
         rows, pos32, cu = meta[:n], meta[n:2 * n], meta[2 * n:]
         max_len = max(lens)
@@ -218,7 +246,7 @@ class PagedDecoder:
             else:
                 t1 = self._decode_rows(dp, rids, t0, pos1, st)
             t01 = torch.stack([t0, t1]).contiguous()
-            buf = torch.empty((2, len(rids)), dtype=torch.long, pin_memory=True)
+            buf = self._pf_out[: 2 * len(rids)].view(2, len(rids))
             # zero-copy D2H: the prefill's end event must not wait behind evict copies
             check(lib.tf_copy_small(C.c_void_p(buf.data_ptr()), C.c_void_p(t01.data_ptr()), buf.numel() * 8,
                                     C.c_void_p(st.cuda_stream)), "tf_copy_small")
@@ -240,10 +268,10 @@ class PagedDecoder:
             if self._graphs and len(batch) <= max(self._graphs) and self.attn_timing is None:
                 nxt = self._decode_graph(dp, list(batch), pos, st)
             else:
-                toks = torch.tensor([self.pending[r] for r in batch], dtype=torch.long).pin_memory()
-                nxt = self._decode_rows(dp, list(batch), toks.to(self.device, non_blocking=True), pos, st)
+                toks = torch.tensor([self.pending[r] for r in batch], dtype=torch.long)
+                nxt = self._decode_rows(dp, list(batch), self._st_tok.to_device(toks, st), pos, st)
             dp.stats["attn_launches"] += self.s.n_layers
-            host = torch.empty(len(batch), dtype=torch.long, pin_memory=True)
+            host = self._dec_out[: len(batch)]
             nxt = nxt.contiguous()
             # sampled ids -> client (D2H of the step's result), zero-copy so the
             # step's end event does not wait behind evict / write-through copies
@@ -359,8 +387,8 @@ class PagedDecoder:
     def _decode_rows(self, dp, rids, tokens, positions, st):
         s = self.s
         B = len(rids)
-        rows = torch.tensor(rids, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
-        pos32 = torch.tensor(positions, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        rp = self._st_rows.to_device(torch.tensor([rids, positions], dtype=torch.int32), st)
+        rows, pos32 = rp[0], rp[1]
         ctx = pos32 + 1
         max_ctx = max(positions) + 1
         need = int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, self.hq))

@@ -31,9 +31,11 @@ GPU's busy time instead of the readers' reading time.
 from __future__ import annotations
 
 import heapq
+import math
 import time
 
 from .engine import (
+    _ORDER,
     CHUNK_TRANSFER_DONE,
     DECODE_ITER_DONE,
     PREFILL_DONE,
@@ -183,6 +185,9 @@ class RealtimeEngine(Engine):
             return False, clock
         done.sort()
         for t, _, what, s0 in done:
+            kind_done = (PREFILL_DONE if self._gpu[0] == "prefill" else DECODE_ITER_DONE) if what == "gpu" \
+                else CHUNK_TRANSFER_DONE
+            self._drain_heap((t, _ORDER[kind_done]))
             self.now = max(self.now, t)
             if what == "gpu":
                 kind, payload = self._gpu[0], self._gpu[1]
@@ -223,12 +228,28 @@ class RealtimeEngine(Engine):
         if self.max_steps is not None and len(self.steps) >= self.max_steps:
             self._stop = True
 
+    def _drain_heap(self, until) -> bool:
+        """Process queued events strictly before ``until`` = (time, kind order):
+        a completion observed late is handled only after every event that
+        precedes it (discrete-event order of the reference, engine.py _ORDER)."""
+        ran = False
+        while self._heap and self._heap[0][:2] < until:
+            t, _, subject, seq = heapq.heappop(self._heap)
+            kind, payload = self._payload.pop(seq)
+            self.now = max(self.now, t)
+            self._last_event_time = self.now
+            self._handlers[kind](t, subject, *payload)
+            ran = True
+            if self.live == 0 or self._stop:
+                break
+        return ran
+
     def run(self):
         for r in self.trace.requests:
             self._push(r.arrival_time, "arrival", r.id)
         self._push(0.0, "schedule_tick", -1)
-        handlers = {"arrival": self._on_arrival, "schedule_tick": self._on_schedule_tick,
-                    "request_done": self._on_request_done, "consume": self._on_consume}
+        self._handlers = {"arrival": self._on_arrival, "schedule_tick": self._on_schedule_tick,
+                          "request_done": self._on_request_done, "consume": self._on_consume}
         self._t0 = time.perf_counter()
         self._reanchor()
         wall0 = time.perf_counter()
@@ -238,15 +259,8 @@ class RealtimeEngine(Engine):
                 self.truncated = True
                 break
             progressed, now = self._poll_completions()
-            while self._heap and self._heap[0][0] <= now:
-                t, _, subject, seq = heapq.heappop(self._heap)
-                kind, payload = self._payload.pop(seq)
-                self.now = max(self.now, t)
-                self._last_event_time = self.now
-                handlers[kind](t, subject, *payload)
+            if self.live > 0 and not self._stop and self._drain_heap((now, math.inf)):
                 progressed = True
-                if self.live == 0 or self._stop:
-                    break
             if progressed:
                 idle_spins = 0
                 continue

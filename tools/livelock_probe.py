@@ -85,11 +85,17 @@ def main():
                          B200Plane(bool(args.fused), tuple(float(x) for x in args.host_ms.split(","))), skip_idle=True, max_wall_s=args.max_wall)
     t0 = time.time()
     res = eng.run()
+    inv = "ok"
+    if not eng.truncated:
+        try:
+            eng._final_invariants(res.records)
+        except Exception as e:  # noqa: BLE001
+            inv = f"{type(e).__name__}: {e}"
     st = collections.Counter(s.status for s in eng.state.values())
     print(json.dumps({"policy": args.policy, "fused": args.fused, "truncated": eng.truncated,
                       "total_time": res.total_time, "preemptions": res.total_preemptions,
                       "recomputes": res.total_recomputes, "steps": len(eng.steps), "wall": time.time() - t0,
-                      "status": dict(st), "event_hash": res.event_hash()[:16]}))
+                      "status": dict(st), "event_hash": res.event_hash()[:16], "invariants": inv}))
 
 
 if __name__ == "__main__":
