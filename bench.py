@@ -413,6 +413,9 @@ def run_ours(args):
     if args.profile_hooks:
         out["host_hook_ms"] = {k: {"calls": c, "avg_ms": round(t / c * 1e3, 4), "total_s": round(t, 3)}
                                for k, (c, t) in dp.hook_time.items() if c}
+        for k, (c, t, ntok) in model.host_s.items():
+            out["host_hook_ms"][f"model.{k}"] = {"calls": c, "avg_ms": round(t / c * 1e3, 4), "total_s": round(t, 3),
+                                                 "avg_tokens": round(ntok / c, 1)}
     if args.dump_ticks:
         import gzip
 

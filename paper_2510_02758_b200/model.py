@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import time
 
 import torch
 from torch.nn.attention.varlen import varlen_attn
@@ -108,10 +109,12 @@ class PagedDecoder:
         self.steps = 0
         self.attn_timing = None  # list -> (algorithmic bytes, start event, end event) per attention launch
         self._st_tok, self._st_meta, self._st_rows = (_Staging(self.device) for _ in range(3))
+        self.host_s = {}  # host-side launch time per phase: name -> [calls, seconds, tokens]
         if self.device.type == "cuda":  # (a CPU-constructed model only serves weight-layout tests)
             self._pf_out = torch.zeros(2 * 4096, dtype=torch.long, pin_memory=True)  # prefill t0 / t1 readback
             self._dec_out = torch.zeros(4096, dtype=torch.long, pin_memory=True)  # sampled ids readback
         self._graphs = {}
+        self._pgraphs = {}  # recompute prefill graphs per token bucket
 
     # ------------------------------------------------------------ pieces
     def prompt_tokens(self, rid: int, n: int) -> torch.Tensor:
@@ -183,7 +186,14 @@ class PagedDecoder:
         meta = self._st_meta.to_device(torch.cat([rows_h, pos_h, cu_h]), st)
         n = toks.numel()
         rows, pos32, cu = meta[:n], meta[n:2 * n], meta[2 * n:]
-        max_len = max(lens)
+        return self._prefill_core(dp, toks, rows, pos32, cu, max(lens), (cu[1:] - 1).long(), st)
+
+    def _prefill_core(self, dp, toks, rows, pos32, cu, max_len, last, st):
+        """Causal forward of the concatenated sequences ``toks`` (device) whose
+        tokens go to (rows, pos32) of the paged pool; cu = cumulative sequence
+        starts (int32, device); returns the argmax after token ``last``."""
+        s = self.s
+        n = toks.numel()
         G = self.hq // self.hkv
         x = self.embed[toks]
         q = torch.empty((n, self.hq, s.head_dim), device=self.device, dtype=x.dtype)
@@ -216,12 +226,21 @@ class PagedDecoder:
             a = varlen_attn(q, kx, vx, cu, cu, max_len, max_len, window_size=(-1, 0)).reshape(n, -1)
             x = self._proj_residual(x, a, L["wo"])
             x = self._mlp(x, L)
-        last = (cu[1:] - 1).long()
         return (self._rms(x[last], self.ln_f) @ self.lm_head).argmax(-1)
 
     @torch.no_grad()
     def prefill(self, dp, job, spans, eng):
         """A prefill job: prompts (+ t0 decode) or recomputes; no host syncs."""
+        t_host = time.perf_counter()
+        try:
+            self._prefill_job(dp, job, spans, eng)
+        finally:
+            h = self.host_s.setdefault("prefill", [0, 0.0, 0])
+            h[0] += 1
+            h[1] += time.perf_counter() - t_host
+            h[2] += sum(hi - lo for _, lo, hi in spans)
+
+    def _prefill_job(self, dp, job, spans, eng):
         st = dp.s_compute
         with torch.cuda.stream(st):
             seqs = []
@@ -230,7 +249,11 @@ class PagedDecoder:
                 prompt = self.prompt_tokens(rid, spec.prompt_len)
                 if job.kind == "recompute":
                     hist = torch.tensor(self.history.get(rid, []), dtype=torch.long)
-                    seqs.append((rid, torch.cat([prompt, hist])[: hi - lo], 0))
+                    toks = torch.cat([prompt, hist])[: hi - lo]
+                    if len(spans) == 1 and self._pgraphs and toks.numel() <= max(self._pgraphs):
+                        self._recompute_graph(dp, rid, toks, st)
+                        return
+                    seqs.append((rid, toks, 0))
                 elif job.kind == "chunk":
                     raise NotImplementedError("chunked prefill (baseline 'chunked' policy) needs prefix attention; "
                                               "use the synthetic KV source for that baseline")
@@ -324,7 +347,7 @@ class PagedDecoder:
         return [(b, e0.elapsed_time(e1)) for b, e0, e1 in res]
 
     # ------------------------------------------------------------ CUDA graphs
-    def enable_graphs(self, dp, buckets=(8, 16, 24, 32, 48, 64, 80, 96, 112, 128)):
+    def enable_graphs(self, dp, buckets=(8, 16, 24, 32, 48, 64, 80, 96, 112, 128), prefill_buckets=512):
         """Capture the decode forward once per batch-size bucket.
 
         Shapes are static per bucket: padded rows point at a scratch table row
@@ -353,6 +376,56 @@ class PagedDecoder:
                 out = self._forward_graphable(dp, io, Bp, ws, torch.cuda.current_stream())
             self._graphs[Bp] = (g, io, stage, out, ws)
         st.synchronize()
+        if prefill_buckets:
+            self._capture_recompute_graphs(dp, mempool, st, prefill_buckets)
+
+    def _capture_recompute_graphs(self, dp, mempool, st, step):
+        """Recompute prefills (one request re-prefilling its whole context,
+        engine.py:889-917) as CUDA graphs per token bucket of ``step`` tokens:
+        the host launches one graph instead of ~400 kernels, so the serving
+        loop stays responsive while the policy is recomputing.  The tail of a
+        bucket is a padding sequence written to the scratch row."""
+        self._pgraphs = {}
+        top = min(dp.max_len, dp.nlb * dp.B)
+        for T in range(step, top + step, step):
+            T = min(T, top)
+            tok = torch.zeros(T, dtype=torch.int64, device=self.device)
+            meta = torch.zeros(2 * T + 3, dtype=torch.int32, device=self.device)
+            last = torch.full((1,), T - 1, dtype=torch.int64, device=self.device)
+            meta[:T] = dp.scratch_row
+            meta[T:2 * T] = torch.arange(T, dtype=torch.int32, device=self.device)
+            meta[2 * T:] = torch.tensor([0, T, T], dtype=torch.int32, device=self.device)
+            rows, pos32, cu = meta[:T], meta[T:2 * T], meta[2 * T:]
+            with torch.cuda.stream(st):
+                self._prefill_core(dp, tok, rows, pos32, cu, T, last, st)  # warm-up
+            st.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=mempool, stream=st):
+                self._prefill_core(dp, tok, rows, pos32, cu, T, last, torch.cuda.current_stream())
+            stage_tok = torch.zeros(T, dtype=torch.int64, pin_memory=True)
+            stage_meta = torch.zeros(2 * T + 3, dtype=torch.int32, pin_memory=True)
+            self._pgraphs[T] = (g, tok, meta, last, stage_tok, stage_meta)
+            if T == top:
+                break
+        st.synchronize()
+
+    def _recompute_graph(self, dp, rid, toks, st):
+        n = toks.numel()
+        T = next(b for b in sorted(self._pgraphs) if b >= n)
+        g, tok, meta, last, stage_tok, stage_meta = self._pgraphs[T]
+        stage_tok[:n] = toks
+        stage_tok[n:] = 0
+        stage_meta[:n] = rid
+        stage_meta[n:T] = dp.scratch_row
+        stage_meta[T:T + n] = torch.arange(n, dtype=torch.int32)
+        stage_meta[T + n:2 * T] = torch.arange(T - n, dtype=torch.int32)
+        stage_meta[2 * T:] = torch.tensor([0, n, T], dtype=torch.int32)
+        with torch.cuda.stream(st):
+            for dst, src in ((tok, stage_tok), (meta, stage_meta)):
+                check(lib.tf_copy_small(C.c_void_p(dst.data_ptr()), C.c_void_p(src.data_ptr()),
+                                        dst.numel() * dst.element_size(), C.c_void_p(st.cuda_stream)),
+                      "tf_copy_small")
+            g.replay()
 
     def _forward_graphable(self, dp, io, Bp, ws, st):
         rows = io[1].to(torch.int32)

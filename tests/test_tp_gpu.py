@@ -141,3 +141,47 @@ def test_prefill_varlen_matches_per_sequence_sdpa(cuda):
     a = pool1.gpu_view()[:used].view(torch.bfloat16).float()
     b = pool2.gpu_view()[:used].view(torch.bfloat16).float()
     assert (a - b).abs().max().item() <= 2e-2 * max(1.0, b.abs().max().item())
+
+
+def test_recompute_prefill_graph_matches_eager(cuda):
+    """A recompute prefill replayed from its token-bucket CUDA graph (padded
+    tail to the scratch row) writes the same paged KV as the eager prefill."""
+    import torch
+
+    from paper_2510_02758_b200 import configs
+    from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
+    from paper_2510_02758_b200.model import PagedDecoder
+    from paper_2510_02758_b200.workload import RequestSpec
+
+    shape = configs.TINY
+    reqs = [RequestSpec(i, 0.0, 60, 60, 20.0) for i in range(2)]
+    nlb = 8
+    outs = []
+    for use_graph in (False, True):
+        pool = KvPool(2 * nlb + 4, 1, shape.n_layers, shape.n_kv_heads, shape.head_dim, device=cuda)
+        pool.gpu.zero_()
+        model = PagedDecoder(shape, device=cuda, seed=5)
+        dp = GpuDataPlane(reqs, pool, mode="realtime", kv_source="model", model=model, n_q_heads=shape.n_q_heads)
+        dp.enable_scratch()  # takes a block from the allocator before the manual mapping below
+        sb = dp.scratch_block
+        free = [b for b in range(pool.n_blocks) if b != sb]
+        dp.table[:2, :nlb] = torch.tensor(free[: 2 * nlb], dtype=torch.int32, device=cuda).view(2, nlb)
+        toks = torch.randint(0, shape.vocab, (77,), generator=torch.Generator().manual_seed(3))
+        st = dp.s_compute
+        if use_graph:
+            model.enable_graphs(dp, buckets=(8,), prefill_buckets=32)
+            with torch.cuda.stream(st):
+                model._recompute_graph(dp, 1, toks, st)
+        else:
+            with torch.cuda.stream(st):
+                model._prefill_batch(dp, [(1, toks, 0)], st)
+        torch.cuda.synchronize()
+        blocks = dp.table[1, : (77 + 15) // 16].long()
+        v = pool.gpu_view()[blocks].view(torch.bfloat16).float()
+        outs.append(v.reshape(v.shape[0], shape.n_layers, 2, shape.n_kv_heads, 16, shape.head_dim))
+    a, b = outs
+    # positions 0..76 (the last block is partial)
+    a = a.permute(0, 4, 1, 2, 3, 5).reshape(-1, shape.n_layers, 2, shape.n_kv_heads, shape.head_dim)[:77]
+    b = b.permute(0, 4, 1, 2, 3, 5).reshape(-1, shape.n_layers, 2, shape.n_kv_heads, shape.head_dim)[:77]
+    # padding changes the GEMM shapes (and so cuBLAS blocking): equal to bf16 noise
+    assert (a - b).abs().max().item() <= 2e-2 * max(1.0, a.abs().max().item())
