@@ -74,10 +74,11 @@ def test_graph_decode_matches_eager(cuda):
     model = PagedDecoder(shape, device=cuda)
     dp = GpuDataPlane(reqs, pool, mode="realtime", kv_source="model", model=model, n_q_heads=shape.n_q_heads)
     # map positions [0, 64) of every request to distinct blocks and fill KV with noise
-    tab = torch.arange(5 * 4, dtype=torch.int32, device=cuda).view(5, 4)
+    dp.enable_scratch()  # the scratch block comes from the allocator: keep it out of the manual mapping
+    free = [b for b in range(64) if b != dp.scratch_block]
+    tab = torch.tensor(free[:20], dtype=torch.int32, device=cuda).view(5, 4)
     dp.table[:5, :4] = tab
     pool.gpu.copy_((torch.randn(pool.gpu.numel(), device=cuda) * 0.3).to(torch.bfloat16).view(torch.int16))
-    dp.enable_scratch()
     model.enable_graphs(dp, buckets=(8,))
     rids, pos = [0, 2, 3], [40, 54, 61]
     for r in rids:
