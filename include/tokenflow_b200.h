@@ -227,6 +227,44 @@ typedef struct {
   double ema_factor;
 } tf_tick_params;
 
+/* On-device snapshot builder input: the engine's raw
+ * per-request counters, ALL requests in request-id order; the device derives
+ * the MemberView rows of tokensim/engine.py:993-1061 (membership = in service
+ * and not generation-complete; t_io = io_overhead_estimate, kvstore.py:173-193;
+ * t_recompute = prefill_s_per_token * total_kv) in the reference's operation
+ * order, compacts them and hands them to the tick kernel without a host
+ * round trip. */
+enum { TF_ST_PENDING = 0, TF_ST_WAITING = 1, TF_ST_PREFILL_WAIT = 2, TF_ST_PREFILLING = 3, TF_ST_RUNNING = 4,
+       TF_ST_PREEMPTED = 5, TF_ST_LOADING = 6, TF_ST_RECOMPUTING = 7, TF_ST_GEN_DONE = 8, TF_ST_DONE = 9 };
+
+typedef struct {
+  int32_t request_id;
+  int32_t status; /* TF_ST_* */
+  int32_t prompt_len;
+  int32_t output_len;
+  int32_t has_tprime;
+  int32_t pad_;
+  int64_t generated;
+  int64_t consumed;
+  int64_t total_kv;
+  int64_t gpu_resident;
+  int64_t cpu_synced;
+  int64_t inflight_d2h;
+  double arrival_time;
+  double rate;
+  double busy_since_tick;
+  double last_iter_time; /* 0.0 encodes None */
+  double t_prime;
+} tf_req_row;
+
+typedef struct {
+  int64_t q_d2h_tokens; /* tokens queued or in service per channel */
+  int64_t q_h2d_tokens;
+  double d2h_rate;      /* measured EMA, or the configured bandwidth before the first sample */
+  double h2d_rate;
+  double prefill_s_per_token;
+} tf_snap_globals;
+
 /* Result arrays (caller-owned host memory, capacity n_members / n_waiting):
  * counts[0]=mode, [1]=n_preempt, [2]=n_resume, [3]=n_admitted,
  * [4]=n_recomputed, [5]=n_batches.  resume_how: 0 load, 1 recompute.
@@ -251,6 +289,12 @@ int tf_selector_init(void* dev_ws, int64_t dev_bytes, void* host_pinned_ws, int6
 int tf_selector_destroy(int64_t sel);
 int tf_policy_tick(int64_t sel, const tf_tick_params* p, const tf_member* members, const tf_waiter* waiting,
                    tf_tick_result* out, void* stream);
+/* on_tick from raw request rows: builds the member view on the device
+ * (p->n_members is ignored and set by the builder); member_ids (capacity
+ * n_rows) receives the request id of every member, in member order. */
+int tf_policy_tick_rows(int64_t sel, const tf_tick_params* p, const tf_req_row* rows, int32_t n_rows,
+                        const tf_snap_globals* g, const tf_waiter* waiting, tf_tick_result* out, int32_t* member_ids,
+                        int32_t* n_members, void* stream);
 int tf_policy_fastpath(int64_t sel, const tf_tick_params* p, const tf_member* members, const tf_waiter* waiting,
                        tf_tick_result* out, void* stream);
 

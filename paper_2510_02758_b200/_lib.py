@@ -43,6 +43,27 @@ class TfMember(C.Structure):
     ]
 
 
+class TfReqRow(C.Structure):
+    _fields_ = [
+        ("request_id", C.c_int32), ("status", C.c_int32), ("prompt_len", C.c_int32), ("output_len", C.c_int32),
+        ("has_tprime", C.c_int32), ("pad_", C.c_int32),
+        ("generated", C.c_int64), ("consumed", C.c_int64), ("total_kv", C.c_int64), ("gpu_resident", C.c_int64),
+        ("cpu_synced", C.c_int64), ("inflight_d2h", C.c_int64),
+        ("arrival_time", C.c_double), ("rate", C.c_double), ("busy_since_tick", C.c_double),
+        ("last_iter_time", C.c_double), ("t_prime", C.c_double),
+    ]
+
+
+class TfSnapGlobals(C.Structure):
+    _fields_ = [("q_d2h_tokens", C.c_int64), ("q_h2d_tokens", C.c_int64), ("d2h_rate", C.c_double),
+                ("h2d_rate", C.c_double), ("prefill_s_per_token", C.c_double)]
+
+
+# engine status -> TF_ST_* (include/tokenflow_b200.h)
+STATUS_CODES = {"waiting": 1, "prefill_wait": 2, "prefilling": 3, "running": 4, "preempted": 5, "loading": 6,
+                "recomputing": 7, "gen_done": 8, "done": 9}
+
+
 class TfWaiter(C.Structure):
     _fields_ = [("request_id", C.c_int32), ("prompt_len", C.c_int32), ("waited_s", C.c_double)]
 
@@ -110,6 +131,9 @@ SIGNATURES = {
     "tf_selector_workspace_bytes": (_I64, [_I32, _I32]),
     "tf_selector_init": (C.c_int, [_P, _I64, _P, _I64, _I32, _I32, C.POINTER(_I64)]),
     "tf_selector_destroy": (C.c_int, [_I64]),
+    "tf_policy_tick_rows": (C.c_int, [_I64, C.POINTER(TfTickParams), C.POINTER(TfReqRow), _I32,
+                                      C.POINTER(TfSnapGlobals), C.POINTER(TfWaiter), C.POINTER(TfTickResult),
+                                      _PI32, _PI32, _P]),
     "tf_policy_tick": (C.c_int, [_I64, C.POINTER(TfTickParams), C.POINTER(TfMember), C.POINTER(TfWaiter),
                                  C.POINTER(TfTickResult), _P]),
     "tf_policy_fastpath": (C.c_int, [_I64, C.POINTER(TfTickParams), C.POINTER(TfMember), C.POINTER(TfWaiter),

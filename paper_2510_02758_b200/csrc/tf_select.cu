@@ -886,8 +886,8 @@ static std::vector<Selector*> g_sel;
 static int64_t align_up(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
 struct Layout {
-  int64_t params, members, waiters, counts, preempt, resume_ids, resume_how, admitted, recomputed, batch_sizes,
-      batch_ids, tprime_out, tprime_set, aux, total;
+  int64_t params, members, waiters, rows, globals, counts, preempt, resume_ids, resume_how, admitted, recomputed,
+      batch_sizes, batch_ids, tprime_out, tprime_set, member_ids, aux, total;
 };
 
 static Layout layout(int32_t max_n, int32_t max_w) {
@@ -901,6 +901,8 @@ static Layout layout(int32_t max_n, int32_t max_w) {
   L.params = take(sizeof(tf_tick_params));
   L.members = take((int64_t)max_n * sizeof(tf_member));
   L.waiters = take((int64_t)max_w * sizeof(tf_waiter));
+  L.rows = take((int64_t)max_n * sizeof(tf_req_row));
+  L.globals = take(sizeof(tf_snap_globals));
   L.counts = take(8 * sizeof(int32_t));
   L.preempt = take((int64_t)max_n * 4);
   L.resume_ids = take((int64_t)max_n * 4);
@@ -911,6 +913,7 @@ static Layout layout(int32_t max_n, int32_t max_w) {
   L.batch_ids = take((int64_t)max_w * 4);
   L.tprime_out = take((int64_t)max_n * 8);
   L.tprime_set = take((int64_t)max_n * 4);
+  L.member_ids = take((int64_t)max_n * 4);
   L.aux = take((int64_t)max_n * 24 + 64);
   L.total = o;
   return L;
@@ -921,8 +924,88 @@ static Selector* get_sel(int64_t h) {
   return g_sel[h - 1];
 }
 
+
+// ------------------------------------------------------------------------
+// On-device snapshot builder (tokensim/engine.py:993-1061 restated): one CTA
+// compacts the in-service, not generation-complete requests in id order and
+// derives their member fields in the reference's float64 operation order
+// (this unit is compiled with -fmad=false, so the four-term t_io sum rounds
+// exactly like CPython).  Writes params.n_members for the tick kernel.
+__device__ __forceinline__ bool st_in_service(int st) { return st >= TF_ST_PREFILL_WAIT && st <= TF_ST_RECOMPUTING; }
+__device__ __forceinline__ bool st_pinned(int st) {
+  return st == TF_ST_PREFILL_WAIT || st == TF_ST_PREFILLING || st == TF_ST_LOADING || st == TF_ST_RECOMPUTING;
+}
+
+__global__ void __launch_bounds__(kSelThreads) snapshot_kernel(const tf_req_row* __restrict__ rows, int n_rows,
+                                                               const tf_snap_globals* __restrict__ g,
+                                                               tf_tick_params* p, tf_member* mem, int32_t* ids,
+                                                               int32_t* counts) {
+  __shared__ int warp_tot[kSelThreads / 32];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const double d2h_rate = g->d2h_rate, h2d_rate = g->h2d_rate, pf = g->prefill_s_per_token;
+  const double qd = (double)g->q_d2h_tokens / d2h_rate, qh = (double)g->q_h2d_tokens / h2d_rate;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int off = 0; off < n_rows; off += kSelThreads) {
+    const int i = off + threadIdx.x;
+    bool take = false;
+    if (i < n_rows) {
+      const tf_req_row& r = rows[i];
+      take = st_in_service(r.status) && !(r.generated >= r.output_len);
+    }
+    // block-wide exclusive scan of the take flags (keeps id order)
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    const int in_warp = __popc(bal & ((1u << lane) - 1));
+    if (lane == 0) warp_tot[warp] = __popc(bal);
+    __syncthreads();
+    int before = base;
+    for (int w = 0; w < warp; ++w) before += warp_tot[w];
+    if (take) {
+      const tf_req_row& r = rows[i];
+      tf_member& m = mem[before + in_warp];
+      m.request_id = r.request_id;
+      m.prompt_len = r.prompt_len;
+      m.output_len = r.output_len;
+      m.running = r.status == TF_ST_RUNNING;
+      m.pinned = st_pinned(r.status);
+      m.has_tprime = r.has_tprime;
+      m.generated = r.generated;
+      m.consumed = r.consumed;
+      m.ctx_tokens = r.total_kv;
+      m.gpu_resident = r.gpu_resident;
+      m.arrival_time = r.arrival_time;
+      m.rate = r.rate;
+      m.busy_since_tick = r.busy_since_tick;
+      long long tail, load;
+      if (r.gpu_resident >= r.total_kv) {
+        tail = load = 0;
+      } else {
+        tail = r.total_kv - r.cpu_synced > 0 ? r.total_kv - r.cpu_synced : 0;
+        load = r.total_kv - r.gpu_resident > 0 ? r.total_kv - r.gpu_resident : 0;
+      }
+      // q_d2h/d2h_rate + tail/d2h_rate + q_h2d/h2d_rate + load/h2d_rate, left to right
+      m.t_io = ((qd + (double)tail / d2h_rate) + qh) + (double)load / h2d_rate;
+      m.t_recompute = pf * (double)r.total_kv;
+      m.last_iter_time = r.last_iter_time;
+      m.t_prime = r.t_prime;
+      ids[before + in_warp] = r.request_id;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 0; w < kSelThreads / 32; ++w) base += warp_tot[w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    p->n_members = base;
+    counts[7] = base;
+  }
+}
+
 static int run_tick(int64_t sel, const tf_tick_params* p, const tf_member* members, const tf_waiter* waiting,
-                    tf_tick_result* out, void* stream, int fastpath) {
+                    tf_tick_result* out, void* stream, int fastpath, const tf_req_row* rows = nullptr,
+                    int32_t n_rows = 0, const tf_snap_globals* g = nullptr, int32_t* member_ids = nullptr,
+                    int32_t* n_members_out = nullptr) {
   Selector* S = get_sel(sel);
   TF_CHECK_ARG(S, "selector: unknown handle");
   TF_CHECK_ARG(p && out && out->counts, "selector: NULL params/result");
@@ -933,14 +1016,29 @@ static int run_tick(int64_t sel, const tf_tick_params* p, const tf_member* membe
   TF_CHECK_ARG(p->per_request_mem_estimate > 0, "per_request_estimate must be > 0");
   TF_CHECK_ARG(p->gpu_mem_total + p->cpu_mem_total >= p->per_request_mem_estimate,
                "total_mem must cover at least one request");
-  const int n = p->n_members, w = p->n_waiting;
+  int n = p->n_members;
+  const int w = p->n_waiting;
   Layout L = layout(S->max_n, S->max_w);
   cudaStream_t st = (cudaStream_t)stream;
   // stage inputs in the pinned host workspace, one H2D copy
   memcpy(S->host + L.params, p, sizeof(*p));
-  if (n) memcpy(S->host + L.members, members, (size_t)n * sizeof(tf_member));
+  if (rows) {
+    TF_CHECK_ARG(n_rows >= 0 && n_rows <= S->max_n, "selector: n_rows %d exceeds capacity %d", n_rows, S->max_n);
+    TF_CHECK_ARG(g && member_ids && n_members_out, "selector: NULL rows-path argument");
+    if (n_rows) memcpy(S->host + L.rows, rows, (size_t)n_rows * sizeof(tf_req_row));
+    memcpy(S->host + L.globals, g, sizeof(*g));
+  } else if (n) {
+    memcpy(S->host + L.members, members, (size_t)n * sizeof(tf_member));
+  }
   if (w) memcpy(S->host + L.waiters, waiting, (size_t)w * sizeof(tf_waiter));
   TF_CUDA(cudaMemcpyAsync(S->dev, S->host, L.counts, cudaMemcpyHostToDevice, st));
+  if (rows) {
+    snapshot_kernel<<<1, kSelThreads, 0, st>>>((const tf_req_row*)(S->dev + L.rows), n_rows,
+                                               (const tf_snap_globals*)(S->dev + L.globals),
+                                               (tf_tick_params*)(S->dev + L.params), (tf_member*)(S->dev + L.members),
+                                               (int32_t*)(S->dev + L.member_ids), (int32_t*)(S->dev + L.counts));
+    TF_LAUNCH_CHECK();
+  }
   TickArgs a;
   a.p = (const tf_tick_params*)(S->dev + L.params);
   a.mem = (const tf_member*)(S->dev + L.members);
@@ -962,6 +1060,11 @@ static int run_tick(int64_t sel, const tf_tick_params* p, const tf_member* membe
   TF_CUDA(cudaStreamSynchronize(st));
   const int32_t* c = (const int32_t*)(S->host + L.counts);
   memcpy(out->counts, c, 6 * sizeof(int32_t));
+  if (rows) {
+    n = c[7];
+    *n_members_out = n;
+    memcpy(member_ids, S->host + L.member_ids, (size_t)n * 4);
+  }
   auto cp = [&](void* dst, int64_t off, int64_t bytes) {
     if (dst && bytes > 0) memcpy(dst, S->host + off, (size_t)bytes);
   };
@@ -1024,6 +1127,14 @@ int tf_selector_destroy(int64_t sel) {
 int tf_policy_tick(int64_t sel, const tf_tick_params* p, const tf_member* members, const tf_waiter* waiting,
                    tf_tick_result* out, void* stream) {
   return run_tick(sel, p, members, waiting, out, stream, 0);
+}
+
+int tf_policy_tick_rows(int64_t sel, const tf_tick_params* p, const tf_req_row* rows, int32_t n_rows,
+                        const tf_snap_globals* g, const tf_waiter* waiting, tf_tick_result* out, int32_t* member_ids,
+                        int32_t* n_members, void* stream) {
+  TF_CHECK_ARG(n_rows == 0 || rows, "tf_policy_tick_rows: NULL rows");
+  static const tf_req_row kNone{};
+  return run_tick(sel, p, nullptr, waiting, out, stream, 0, rows ? rows : &kNone, n_rows, g, member_ids, n_members);
 }
 
 int tf_policy_fastpath(int64_t sel, const tf_tick_params* p, const tf_member* members, const tf_waiter* waiting,

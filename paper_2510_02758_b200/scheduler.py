@@ -226,6 +226,32 @@ class SystemSnapshot:
 
 
 @dataclass
+class RowsSnapshot:
+    """A SystemSnapshot whose member view is built ON THE DEVICE:
+    the engine ships its raw per-request counters (``rows``: tf_req_row, every
+    request in id order) and the queue / rate globals; tf_policy_tick_rows
+    derives the MemberView fields, compacts the members and runs the tick
+    with no host round trip.  ``materialize`` is the host equivalent (for
+    host-side policies and tests)."""
+
+    now: float
+    rows: object
+    n_rows: int
+    globals: object
+    waiting: list
+    free_slots: int
+    gpu_mem_free: float
+    gpu_mem_total: float
+    cpu_mem_total: float
+    max_batch: int
+    gamma: float
+    prefill_s_per_token: float
+    offload_enabled: bool
+    h2d_blocked_tokens: int = 0
+    materialize: object = None
+
+
+@dataclass
 class TickDecision:
     mode: str
     preempt: list = field(default_factory=list)
@@ -291,8 +317,13 @@ class BufferAwarePolicy(Policy):
             self.mode_changes.append((now, mode))
         self.mode = mode
 
-    def on_tick(self, view: SystemSnapshot) -> TickDecision:
-        mode, pre, resume, adm, rc, batches = self.selector.tick(view, self.cfg, self._t_prime, self.mode)
+    device_snapshot = True  # the engine may hand on_tick a RowsSnapshot
+
+    def on_tick(self, view) -> TickDecision:
+        if isinstance(view, RowsSnapshot):
+            mode, pre, resume, adm, rc, batches = self.selector.tick_rows(view, self.cfg, self._t_prime, self.mode)
+        else:
+            mode, pre, resume, adm, rc, batches = self.selector.tick(view, self.cfg, self._t_prime, self.mode)
         self.set_mode(view.now, mode)
         self.preemption_count += len(pre)
         return TickDecision(mode=mode, preempt=pre, resume=resume, prefill_batches=batches,

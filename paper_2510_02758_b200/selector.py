@@ -12,7 +12,7 @@ import ctypes as C
 import torch
 
 from . import _lib
-from ._lib import TfMember, TfPrio, TfTickParams, TfTickResult, TfWaiter, check, lib
+from ._lib import TfMember, TfPrio, TfReqRow, TfSnapGlobals, TfTickParams, TfTickResult, TfWaiter, check, lib
 
 MODE_CODES = {"buffer_aware": 0, "fcfs_fallback": 1}
 MODE_NAMES = {v: k for k, v in MODE_CODES.items()}
@@ -44,7 +44,8 @@ class GpuSelector:
     # ------------------------------------------------------------------ packing
     def _params(self, snap, cfg, mode_code: int) -> TfTickParams:
         p = TfTickParams()
-        p.n_members, p.n_waiting = len(snap.members), len(snap.waiting)
+        p.n_members = 0 if hasattr(snap, "rows") else len(snap.members)
+        p.n_waiting = len(snap.waiting)
         if p.n_members > self.max_n or p.n_waiting > self.max_w:
             raise ValueError("snapshot exceeds selector capacity")
         p.free_slots, p.max_batch = snap.free_slots, snap.max_batch
@@ -93,6 +94,32 @@ class GpuSelector:
         for i, m in enumerate(snap.members):
             if self._res["t_prime_set"][i]:
                 t_prime[m.request_id] = self._tp[i]
+        return self._unpack()
+
+    def tick_rows(self, snap, cfg, t_prime: dict, mode: str):
+        """on_tick from a RowsSnapshot: the member view is built on the device
+        (tf_policy_tick_rows); t_prime is filled into the rows here."""
+        rows = snap.rows
+        for i in range(snap.n_rows):
+            r = rows[i]
+            tp = t_prime.get(r.request_id)
+            r.has_tprime = int(tp is not None)
+            r.t_prime = tp if tp is not None else 0.0
+        for i, w in enumerate(snap.waiting):
+            d = self._waiters[i]
+            d.request_id, d.prompt_len, d.waited_s = w.request_id, w.prompt_len, w.waited_s
+        p = self._params(snap, cfg, MODE_CODES[mode])
+        p.n_members = 0
+        r = self._result()
+        ids = (C.c_int32 * max(1, snap.n_rows))()
+        nm = C.c_int32()
+        check(lib.tf_policy_tick_rows(self.handle, C.byref(p), rows, snap.n_rows, C.byref(snap.globals),
+                                      self._waiters, C.byref(r), ids, C.byref(nm),
+                                      C.c_void_p(_lib.stream_ptr(self.stream))), "tf_policy_tick_rows")
+        self.calls += 1
+        for i in range(nm.value):
+            if self._res["t_prime_set"][i]:
+                t_prime[ids[i]] = self._tp[i]
         return self._unpack()
 
     def fastpath(self, snap, cfg, mode: str):

@@ -114,3 +114,28 @@ def test_select_batch_large_random(sel):
             lengths[i] = rng.randint(100, 3000)
         mem = int(sum(lengths.values()) * 0.3)
         assert sel.select_batch(views, mem, n // 3, lengths) == choose_batch(views, mem, n // 3, lengths)
+
+
+@pytest.mark.parametrize("name", ["c1_tokenflow", "table2_s3_full", "c2_burst256_s1_tokenflow"])
+def test_device_snapshot_builder_matches_reference(sel, name):
+    """with the member view built on the device from the raw
+    request counters (tf_policy_tick_rows), the runtime reproduces the
+    reference's event hash and decision log - same as the host-built view."""
+    from conftest import trace_path
+
+    from paper_2510_02758_b200.costs import CostModel
+    from paper_2510_02758_b200.engine import Engine, SimConfig
+    from paper_2510_02758_b200.scheduler import SchedulerConfig, make_policy
+    from paper_2510_02758_b200.workload import load_trace
+
+    g = load_golden("runs", name)
+    tr = load_trace(trace_path(g["trace"]))
+    hashes = []
+    for device in (True, False):
+        eng = Engine(tr, make_policy(g["policy"], SchedulerConfig(**g["sched"])), CostModel(**g["cm"]),
+                     SimConfig(**g["sim"]))
+        eng.device_snapshot = device
+        res = eng.run()
+        assert res.decision_log == g["decision_log"], f"device_snapshot={device}"
+        hashes.append(res.event_hash())
+    assert hashes[0] == hashes[1] == g["event_hash"]
