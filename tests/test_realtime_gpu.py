@@ -48,7 +48,11 @@ def test_realtime_c1_completes_with_invariants(cuda, engine, graphs, fused):
         assert dp.stats["d2h_launches"] < 0.2 * dp.stats["decode_steps"]
     eng._final_invariants(res.records)
     assert all(len(r.gen_times) == r.output_len for r in res.records)
-    assert res.total_preemptions > 0 and dp.stats["h2d_tokens"] > 0
+    # preempted requests come back by load or - when the measured prefill rate
+    # makes it cheaper (graph-replayed recomputes of the tiny model) - recompute
+    assert res.total_preemptions > 0 and (dp.stats["h2d_tokens"] > 0 or res.total_recomputes > 0)
+    if not graphs:
+        assert dp.stats["h2d_tokens"] > 0
     # fused: every KV position is mirrored by the epilogue that produced it, so
     # no separate write-through / evict chunk may be needed at all
     assert dp.stats["d2h_tokens"] > 0 or fused
