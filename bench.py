@@ -223,12 +223,13 @@ def run_ours(args):
     def window_probes(eng, timed):
         """Right at the end of the timed window (device idle, live batch intact):
         the roofline of the dominant kernel (paged attention re-launched on the
-        largest timed batch's still-resident members, all layers, CUDA events)
-        and transfer hidden under the captured decode of that batch."""
+        running batch, all layers, CUDA events) and transfer hidden under the
+        captured decode of that batch."""
         torch.cuda.synchronize()
         hbm, peak_kind = _peaks()
-        big = max(timed, key=lambda r: r["batch"])
-        live = [r for r in big["rids"] if eng.state[r].status == "running"]
+        # the decode batch at the window's end: every running request (what the
+        # next step would read), capped at max_batch
+        live = sorted(r for r in eng.running if eng.state[r].status == "running")[: c2.max_batch]
         if not live:
             return
         per = model.measure_attention(dp, live, [eng.state[r].kv.total_kv - 1 for r in live])
@@ -246,8 +247,8 @@ def run_ours(args):
                          "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live),
                          "algorithmic_bytes_per_launch": round(avg_bytes),
                          "note": f"bytes = sum(ctx) x {pool.H * pool.D * 4} B (K+V, {pool.H} kv heads x {pool.D} x "
-                                 "bf16) + q/out + table entries per layer; re-launched on the window's largest "
-                                 "batch right after the window"}
+                                 "bf16) + q/out + table entries per layer; re-launched right after the window on "
+                                 "the running batch"}
         if args.graphs:
             xf = dp.transfer_log()[state["ev0"]:state["ev1"]]
             per_step = lambda k: math.ceil(sum(n for d, n, _ in xf if d == k) / 16 / len(timed))  # noqa: E731
