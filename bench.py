@@ -333,6 +333,9 @@ def run_ours(args):
     h2d_tok = sum(n for k, n, _ in xfers if k == "h2d")
     d2h_ms = sum(ms for k, _, ms in xfers if k == "d2h")
     h2d_ms = sum(ms for k, _, ms in xfers if k == "h2d")
+    if world > 1 and not tp_mode:  # C3: every replica's own link, rates over all replicas' chunks
+        d2h_tok, h2d_tok = int(_sum_over_ranks(d2h_tok, world, dev)), int(_sum_over_ranks(h2d_tok, world, dev))
+        d2h_ms, h2d_ms = _sum_over_ranks(d2h_ms, world, dev), _sum_over_ranks(h2d_ms, world, dev)
     swap = {"d2h_tokens": d2h_tok, "h2d_tokens": h2d_tok, "chunks": len(xfers),
             "engine": {0: "SM kernel", 1: "copy-engine batch", 2: "auto (CE whole blocks + SM partial)"}[
                 args.swap_engine],
@@ -386,12 +389,7 @@ def run_ours(args):
         "clocks": sampler.summary(),
         "gpu_launches": None,
         "first_tokens_in_window": len(ttft),
-        "ttft": ({"p99_s": round(ttft_latency_stats(ttft)["p99"], 4), "p50_s": round(ttft_latency_stats(ttft)["p50"], 4),
-                  "mean_s": round(ttft_latency_stats(ttft)["mean"], 4), "requests": len(ttft),
-                  "of": len(res.records), "complete": len(ttft) == len(res.records),
-                  "note": "TTFT latency = first token - arrival (nearest-rank P99, tokensim/metrics.py:144-155), "
-                          "real-time serving continued after the window until every request had its first token"}
-                 if ttft else None),
+        "ttft": _ttft_summary(ttft, len(res.records), world, tp_mode),
     }
     # this package's kernels per decode step: per layer the fused rope/append,
     # paged attention (+ split combine for v3), two RMSNorms and the SwiGLU;
@@ -431,6 +429,29 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return out
+
+
+def _ttft_summary(recs, n_records, world, tp_mode):
+    """TTFT latency stats (first token - arrival, nearest-rank P99,
+    tokensim/metrics.py:144-155) over ALL replicas' requests (C3: gathered)."""
+    from paper_2510_02758_b200.metrics import nearest_rank
+
+    lat = [r.gen_times[0] - r.arrival for r in recs]
+    total = n_records
+    if world > 1 and not tp_mode:
+        import torch.distributed as dist
+
+        parts = [None] * world
+        dist.all_gather_object(parts, (lat, n_records))
+        lat = [x for p in parts for x in p[0]]
+        total = sum(p[1] for p in parts)
+    if not lat:
+        return None
+    v = sorted(lat)
+    return {"p99_s": round(nearest_rank(v, 99.0), 4), "p50_s": round(nearest_rank(v, 50.0), 4),
+            "mean_s": round(sum(v) / len(v), 4), "requests": len(v), "of": total, "complete": len(v) == total,
+            "note": "TTFT latency = first token - arrival (nearest-rank P99, tokensim/metrics.py:144-155), "
+                    "real-time serving continued after the window until every request had its first token"}
 
 
 def _ncu_traffic(alg_bytes):

@@ -185,3 +185,77 @@ def test_recompute_prefill_graph_matches_eager(cuda):
     b = b.permute(0, 4, 1, 2, 3, 5).reshape(-1, shape.n_layers, 2, shape.n_kv_heads, shape.head_dim)[:77]
     # padding changes the GEMM shapes (and so cuBLAS blocking): equal to bf16 noise
     assert (a - b).abs().max().item() <= 2e-2 * max(1.0, a.abs().max().item())
+
+
+def _tp2_worker(rank, port, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # both ranks share cuda:0 here, so the data-path all-reduce runs over gloo
+    # (NCCL needs one device per rank); the kernels and engine are the product's
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    from conftest import load_golden, pool_blocks, trace_path
+
+    from paper_2510_02758_b200 import configs
+    from paper_2510_02758_b200.costs import CostModel
+    from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
+    from paper_2510_02758_b200.engine import SimConfig
+    from paper_2510_02758_b200.model import PagedDecoder
+    from paper_2510_02758_b200.realtime import RealtimeEngine
+    from paper_2510_02758_b200.scheduler import SchedulerConfig, make_policy
+    from paper_2510_02758_b200.tp import Lockstep, TpGroup
+    from paper_2510_02758_b200.workload import load_trace
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    g = load_golden("runs", "c1_tokenflow")
+    tr = load_trace(trace_path(g["trace"]))
+    shape = configs.TINY
+    pool = KvPool(pool_blocks(g["sim"], len(tr.requests)), 4096, shape.n_layers, shape.n_kv_heads // 2,
+                  shape.head_dim, device=dev)
+    model = PagedDecoder(shape, device=dev, seed=0, tp=TpGroup(rank, 2))
+    dp = GpuDataPlane(tr.requests, pool, mode="realtime", kv_source="model", model=model,
+                      n_q_heads=shape.n_q_heads // 2, engine=2)
+    ls = Lockstep(dist.new_group(backend="gloo"))
+    eng = RealtimeEngine(tr, make_policy("tokenflow", SchedulerConfig(**g["sched"])), CostModel(**g["cm"]),
+                         SimConfig(**g["sim"]), dp, skip_idle=True, lockstep=ls)
+    res = eng.run()
+    eng._final_invariants(res.records)
+    same = ls.same(res.event_hash())
+    hist = {r: list(v) for r, v in model.history.items()}
+    parts = [None, None]
+    dist.all_gather_object(parts, {"hash": res.event_hash(), "same": same, "pre": res.total_preemptions,
+                                   "h2d": dp.stats["h2d_tokens"], "hist": hist})
+    if rank == 0:
+        out.put(parts)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_tp2_lockstep_serving_on_one_gpu(cuda):
+    """C4 end to end with TP=2 (two processes sharing one B200): sharded model,
+    per-rank KV pools and swaps, lockstep real-time engines, GPU selector.
+    Both ranks must take the identical event sequence and emit the same tokens."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_tp2_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    a, b = q.get(timeout=900)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert a["same"] and b["same"] and a["hash"] == b["hash"]
+    assert a["pre"] > 0 and a["h2d"] > 0
+    assert a["hist"] == b["hist"], "TP ranks emitted different tokens"
