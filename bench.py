@@ -450,8 +450,9 @@ def _ttft_summary(recs, n_records, world, tp_mode):
     v = sorted(lat)
     return {"p99_s": round(nearest_rank(v, 99.0), 4), "p50_s": round(nearest_rank(v, 50.0), 4),
             "mean_s": round(sum(v) / len(v), 4), "requests": len(v), "of": total, "complete": len(v) == total,
-            "note": "TTFT latency = first token - arrival (nearest-rank P99, tokensim/metrics.py:144-155), "
-                    "real-time serving continued after the window until every request had its first token"}
+            "note": "TTFT latency = first token - arrival (nearest-rank P99, tokensim/metrics.py:144-155)" + (
+                ", real-time serving continued after the window until every request had its first token"
+                if len(v) == total else ", requests that had their first token by the end of the run")}
 
 
 def _ncu_traffic(alg_bytes):
@@ -577,7 +578,10 @@ def run_reference(args):
     out = {"metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
            "data": "synthetic", "impl": "reference",
-           "config": {"workload": "C2 decode step on the host CPU (oracle restatement)", "model": "llama3-8b"},
+           "config": {"workload": "C2: Llama3-8B bf16 random-init, 256-request burst (the same population and "
+                                  "metric as the ours arm); the reference's CPU path = the oracle restatement of one "
+                                  "decode step of the C2 batch on the host cores (tokensim itself has no tensors)",
+                      "model": "llama3-8b", "parallelism": "host CPU"},
            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
                                        "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
