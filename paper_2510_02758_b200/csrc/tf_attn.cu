@@ -49,6 +49,7 @@ struct AttnArgs {
   uint16_t* out;
   int64_t block_elems;
   int32_t stride, n_layers, kv_heads, layer, hq, splits, blocks_per_split;
+  int32_t min_blocks_per_split;  // v3: per-request split size = max(this, ceil(nblk_b / splits))
   float scale_log2;
   // v4 (stream-K): batch, partial slots per (request, kv head), self-resetting counters
   int32_t B, kmax;
@@ -616,8 +617,11 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
   const int split = blockIdx.x;
   const int ctx = a.ctx[b];
   const int nblk = (ctx + kBlk - 1) / kBlk;
-  const int blk_lo = split * a.blocks_per_split;
-  const int blk_hi = min(nblk, blk_lo + a.blocks_per_split);
+  // split size per request: a short request in a launch planned for a long
+  // maximum context still spreads over all splits instead of idling them
+  const int bps = max(a.min_blocks_per_split, (nblk + a.splits - 1) / a.splits);
+  const int blk_lo = split * bps;
+  const int blk_hi = min(nblk, blk_lo + bps);
   const int nmine = blk_hi > blk_lo + warp ? (blk_hi - blk_lo - warp + kV3Warps - 1) / kV3Warps : 0;
 
   const int64_t tile = (int64_t)kBlk * D;
@@ -1138,6 +1142,8 @@ static int v3_stages() {
   return st;
 }
 
+static int g_minblk = 8;
+
 static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps) {
   const int nblk = std::max(1, (max_ctx + kBlk - 1) / kBlk);
   const int base = std::max(1, B * kv_heads);
@@ -1150,6 +1156,7 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
     const char* m = getenv("TF_ATTN_MINBLK");
     waves = w ? std::max(1, atoi(w)) : 2;  // tuned: profiles/r1_attn_plan_tuning.json
     minblk = m ? std::max(1, atoi(m)) : 8;
+    g_minblk = minblk;
   }
   const int per_sm = attn_impl() >= 3 ? (v3_stages() == 2 ? 3 : 2) : 2;  // resident CTAs per SM
   const int target = attn_impl() >= 2 ? 148 * per_sm * waves : 148 * 6;
@@ -1289,6 +1296,7 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
     a.blocks_per_split = 0;
   } else {
   plan_splits(B, p->kv_heads, max_ctx, &a.splits, &a.blocks_per_split);
+  a.min_blocks_per_split = g_minblk;
   int64_t need = a.splits == 1 ? 0 : (int64_t)B * n_q_heads * a.splits * (p->head_dim + 2) * (int64_t)sizeof(float);
   TF_CHECK_ARG(workspace_bytes >= need && (need == 0 || workspace), "tf_paged_decode_attn: workspace too small (%lld < %lld)",
                (long long)workspace_bytes, (long long)need);
