@@ -114,9 +114,12 @@ class GpuDataPlane:
         self.max_len = max(r.prompt_len + r.output_len + 2 for r in reqs)
         self.nlb = (self.max_len + self.B - 1) // self.B
         n_rows = max(r.id for r in reqs) + 1
-        self.flags = {r.id: np.zeros(self.nlb * self.B, np.uint8) for r in reqs}
-        self.gtab = {r.id: np.full(self.nlb, -1, np.int32) for r in reqs}
-        self.htab = {r.id: np.full(self.nlb, -1, np.int32) for r in reqs}
+        # one row per request id (rows are per-request views: flags[rid], gtab[rid]);
+        # 2-D so a decode step's per-member updates are single vectorised ops
+        n_ids = max(r.id for r in reqs) + 1
+        self.flags = np.zeros((n_ids, self.nlb * self.B), np.uint8)
+        self.gtab = np.full((n_ids, self.nlb), -1, np.int32)
+        self.htab = np.full((n_ids, self.nlb), -1, np.int32)
         self.host_hi = {r.id: 0 for r in reqs}
         # one extra row: padding rows of graph-captured decode steps point there
         self.table = torch.full((n_rows + 1, self.nlb), -1, dtype=torch.int32, device=dev)
@@ -313,22 +316,26 @@ class GpuDataPlane:
             self.model.fill_commit(rid)
 
     def decode_start(self, batch, eng):
-        spans = []
-        for rid in batch:
-            p = eng.state[rid].kv.total_kv
-            f = self.flags[rid]
-            if eng.debug_checks and not (f[:p] & LIVE).all():
-                raise _lib.InvariantError(f"decode of {rid} reads non-resident KV")
-            f[p] |= RESERVED
-            self._appending[rid] = p
-            if p % self.B == 0 or self.gtab[rid][p // self.B] < 0:
-                self._reconcile(rid, [p // self.B])
-            if self.fused_wt:
-                j = p // self.B
-                if self.htab[rid][j] < 0:
-                    self.htab[rid][j] = self.pool.alloc(TIER_HOST, 1)[0]
-                    self._pending_htable.append((rid, j, int(self.htab[rid][j])))
-            spans.append((rid, p, p + 1))
+        n = len(batch)
+        rids = np.fromiter(batch, np.int64, n)
+        pos = np.fromiter((eng.state[r].kv.total_kv for r in batch), np.int64, n)
+        if eng.debug_checks:
+            for rid, p in zip(batch, pos.tolist()):
+                if not (self.flags[rid][:p] & LIVE).all():
+                    raise _lib.InvariantError(f"decode of {rid} reads non-resident KV")
+        self.flags[rids, pos] |= RESERVED
+        self._appending.update(zip(batch, pos.tolist()))
+        j = pos // self.B
+        need = (pos % self.B == 0) | (self.gtab[rids, j] < 0)
+        for rid, jj in zip(rids[need].tolist(), j[need].tolist()):
+            self._reconcile(rid, [jj])
+        if self.fused_wt:
+            for rid, jj in zip(batch, j.tolist()):
+                if self.htab[rid][jj] < 0:
+                    self.htab[rid][jj] = self.pool.alloc(TIER_HOST, 1)[0]
+                    self._pending_htable.append((rid, jj, int(self.htab[rid][jj])))
+        pl = pos.tolist()
+        spans = [(rid, p, p + 1) for rid, p in zip(batch, pl)]
         self.stats["append_tokens"] += len(batch)
         self.stats["decode_steps"] += 1
         self._wait_d2h_of(spans, self.s_compute)
@@ -345,16 +352,22 @@ class GpuDataPlane:
         made = set(made)
         if self.model is not None and self.kv_source == "model":
             self.model.decode_commit(made)
-        for rid in batch:
-            f = self.flags[rid]
-            p = self._appending.pop(rid)  # the one position this step reserved
-            if self.fused_wt and rid in made:
-                f[p] |= HOSTV  # mirrored to the host by the fused epilogue
-                self.host_hi[rid] = max(self.host_hi[rid], p + 1)
-            if rid in made:
-                f[p] = (f[p] & CLR_RESERVED) | LIVE
-            else:
-                f[p] &= CLR_RESERVED
+        n = len(batch)
+        rids = np.fromiter(batch, np.int64, n)
+        pos = np.fromiter((self._appending.pop(r) for r in batch), np.int64, n)  # the slot each reserved
+        ok = np.fromiter((r in made for r in batch), bool, n)
+        F = self.flags
+        if ok.any():
+            r1, p1 = rids[ok], pos[ok]
+            if self.fused_wt:
+                F[r1, p1] |= HOSTV  # mirrored to the host by the fused epilogue
+                for rid, p in zip(r1.tolist(), p1.tolist()):
+                    self.host_hi[rid] = max(self.host_hi[rid], p + 1)
+            F[r1, p1] = (F[r1, p1] & CLR_RESERVED) | LIVE
+        if not ok.all():
+            r0, p0 = rids[~ok], pos[~ok]
+            F[r0, p0] &= CLR_RESERVED
+            for rid, p in zip(r0.tolist(), p0.tolist()):
                 self._reconcile(rid, (p // self.B,))
 
     def d2h_start(self, ch, eng):
