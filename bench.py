@@ -500,7 +500,7 @@ def _start_watchdog(eng, dp, period):
     threading.Thread(target=loop, daemon=True).start()
 
 
-def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=24):
+def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=48):
     """Transfer hidden under decode: the real decode step (the
     captured Llama3-8B forward of the live batch) S times alone, the swap
     traffic alone (``blocks_out`` 2 MiB blocks gathered to pinned host on the
