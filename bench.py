@@ -500,7 +500,7 @@ def _start_watchdog(eng, dp, period):
     threading.Thread(target=loop, daemon=True).start()
 
 
-def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=48):
+def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=24):
     """Transfer hidden under decode: the real decode step (the
     captured Llama3-8B forward of the live batch) S times alone, the swap
     traffic alone (``blocks_out`` 2 MiB blocks gathered to pinned host on the
@@ -538,8 +538,6 @@ def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=48):
                                                   C.c_void_p(dp.s_load.cuda_stream)))
 
     def run(fns):
-        for f in fns:
-            f()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(steps):
@@ -548,16 +546,25 @@ def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=48):
         torch.cuda.synchronize()
         return (time.perf_counter() - t0) / steps
 
-    t_dec = run([decode])
-    t_swp = run([swaps])
-    t_both = run([decode, swaps])
+    for f in (decode, swaps):  # warm-up
+        f()
+    # alternate the three measurements over several rounds and take medians:
+    # a small swap volume makes the difference T_both - T_decode tiny, so
+    # drift between separate runs would otherwise dominate it
+    rounds = {"dec": [], "swp": [], "both": []}
+    for _ in range(5):
+        rounds["dec"].append(run([decode]))
+        rounds["both"].append(run([decode, swaps]))
+        rounds["swp"].append(run([swaps]))
+    t_dec, t_swp, t_both = (statistics.median(rounds[k]) for k in ("dec", "swp", "both"))
     pool.free(_lib.TIER_GPU, g)
     pool.free(_lib.TIER_HOST, h)
     return {"blocks_out_per_step": blocks_out, "blocks_in_per_step": blocks_in, "batch": len(rids),
             "t_decode_ms": round(t_dec * 1e3, 3), "t_swap_ms": round(t_swp * 1e3, 3),
             "t_both_ms": round(t_both * 1e3, 3),
             "swap_gbs": round((blocks_out + blocks_in) * pool.block_bytes / t_swp / 1e9, 2),
-            "hidden_frac": round(1.0 - max(0.0, t_both - t_dec) / t_swp, 4)}
+            "hidden_frac": round(min(1.0, 1.0 - max(0.0, t_both - t_dec) / t_swp), 4),
+            "method": "median of 5 alternating rounds of 24 steps each (decode alone / both / swaps alone)"}
 
 
 def cpu_baseline(args, timed, quick=False):
