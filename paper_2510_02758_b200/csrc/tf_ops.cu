@@ -6,6 +6,8 @@
 //   tf_rmsnorm     y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w   (one CTA per row,
 //                  16-B vector loads, fp32 sum, row held in registers)
 //   tf_silu_mul    y = silu(gu[:, :F]) * gu[:, F:]                (one pass, 16-B vectors)
+#include <algorithm>
+
 #include "tf_common.cuh"
 
 namespace tf {
@@ -72,24 +74,24 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* _
   }
 }
 
+// blockIdx.y = row, threads stride the row's 16-B vectors (no 64-bit division)
 __global__ void silu_mul_kernel(const uint16_t* __restrict__ gu, uint16_t* __restrict__ y, int64_t rows, int F) {
   const int nvr = F / 8;  // vectors per output row
-  const int64_t total = rows * nvr;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = t / nvr;
-    const int c = (int)(t % nvr);
-    const uint4* gp = reinterpret_cast<const uint4*>(gu + r * 2 * (int64_t)F) + c;
-    const uint4* up = reinterpret_cast<const uint4*>(gu + r * 2 * (int64_t)F + F) + c;
+  const int64_t r = blockIdx.y;
+  const uint4* gp = reinterpret_cast<const uint4*>(gu + r * 2 * (int64_t)F);
+  const uint4* up = reinterpret_cast<const uint4*>(gu + r * 2 * (int64_t)F + F);
+  uint4* yp = reinterpret_cast<uint4*>(y + r * (int64_t)F);
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nvr; c += gridDim.x * blockDim.x) {
     float g[8], u[8], o[8];
-    unpack8(*gp, g);
-    unpack8(*up, u);
+    unpack8(__ldg(gp + c), g);
+    unpack8(__ldg(up + c), u);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       // torch: silu in fp32, rounded to bf16, then the bf16 product
       const float s = __bfloat162float(__float2bfloat16_rn(g[e] / (1.f + __expf(-g[e]))));
       o[e] = s * u[e];
     }
-    reinterpret_cast<uint4*>(y + r * (int64_t)F)[c] = pack8(o);
+    yp[c] = pack8(o);
   }
 }
 
@@ -114,10 +116,14 @@ int tf_silu_mul(const void* gu, void* y, int32_t rows, int32_t ffn, void* stream
   TF_CHECK_ARG(rows >= 0 && ffn > 0 && ffn % 8 == 0, "tf_silu_mul: bad shape %d x %d", rows, ffn);
   if (rows == 0) return TF_OK;
   TF_CHECK_ARG(gu && y, "tf_silu_mul: NULL pointer");
-  const int64_t total = (int64_t)rows * (ffn / 8);
-  const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  silu_mul_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)gu, (uint16_t*)y, rows, ffn);
-  TF_LAUNCH_CHECK();
+  const int nvr = ffn / 8;
+  for (int32_t r0 = 0; r0 < rows; r0 += 65535) {  // grid.y limit (prefills of > 64K tokens)
+    const int32_t nr = rows - r0 < 65535 ? rows - r0 : 65535;
+    dim3 grid((unsigned)std::max(1, std::min((nvr + 255) / 256, 64)), (unsigned)nr);
+    silu_mul_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)gu + (int64_t)r0 * 2 * ffn,
+                                                            (uint16_t*)y + (int64_t)r0 * ffn, nr, ffn);
+    TF_LAUNCH_CHECK();
+  }
   return TF_OK;
 }
 

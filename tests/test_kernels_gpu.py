@@ -214,7 +214,7 @@ def test_rmsnorm_vs_torch(cuda, rows, dim):
     assert ((y.float() - ref).abs() <= 2 ** -6 * ref.abs() + 1e-3).all()
 
 
-@pytest.mark.parametrize("rows,ffn", [(1, 688), (64, 14336), (200, 3456)])
+@pytest.mark.parametrize("rows,ffn", [(1, 688), (64, 14336), (200, 3456), (70000, 16)])
 def test_silu_mul_vs_torch(cuda, rows, ffn):
     import torch.nn.functional as F
 
