@@ -276,9 +276,12 @@ class RealtimeEngine(Engine):
                     else:
                         time.sleep(min(gap, 0.01))
             else:
+                # waiting on the device: keep polling (a timed sleep oversleeps by
+                # ~50 us, which would sit between every job and the next
+                # dispatch); yield the GIL now and then for the clock sampler
                 idle_spins += 1
-                if idle_spins > 64:
-                    time.sleep(20e-6)
+                if idle_spins % 256 == 0:
+                    time.sleep(0)
         self.dp.synchronize()
         self.wall_s = time.perf_counter() - wall0
         self._last_event_time = max(self._last_event_time, self.now)
