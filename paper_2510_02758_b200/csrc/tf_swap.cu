@@ -213,16 +213,6 @@ static int swap_entry(int64_t pool, const tf_seg* segs, int32_t n, int32_t l0, i
   cudaStream_t st = (cudaStream_t)stream;
   if (engine == TF_ENGINE_CE) return swap_ce(*p, segs, n, l0, l1, to_host, st);
   if (engine == TF_ENGINE_AUTO) {
-    // small chunks with a partial block (write-through tails): one SM kernel
-    // for everything - a copy-engine batch in front of it costs more latency
-    // than its whole blocks save (profiles/r1_wt_chunks.json: <= 64 tokens)
-    int64_t slots = 0;
-    bool partial = false;
-    for (int32_t i = 0; i < n; ++i) {
-      slots += segs[i].n_slots;
-      partial |= segs[i].n_slots != p->block_tokens;
-    }
-    if (partial && slots <= 4 * p->block_tokens) return swap_sm(*p, segs, n, l0, l1, to_host, st);
     // whole blocks (one contiguous run each) -> copy engines, no SMs;
     // partial blocks (2*kv_heads*layers short runs each) -> one SM kernel
     std::vector<tf_seg> full, part;
