@@ -600,8 +600,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 // S = ring stages per warp (S - 1 blocks in flight); 2 stages fit 3 CTAs per
 // SM (12 warps), 3 stages 2 CTAs per SM (8 warps).
-template <int G, int S, int W = kV3Warps>
-__global__ void __launch_bounds__(W * 32, W == 2 ? 4 : (S == 2 ? 3 : 2)) paged_attn_mma_kernel(const AttnArgs a) {
+template <int G, int S>
+__global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_kernel(const AttnArgs a) {
   constexpr int D = 128;
   static_assert(G >= 1 && G <= 8, "v3 packs the group into rows 0..7 of the 16-row tile");
   static_assert(S >= 2 && S <= 4, "2..4 stages");
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(W * 32, W == 2 ? 4 : (S == 2 ? 3 : 2)) paged_a
   const int bps = max(a.min_blocks_per_split, (nblk + a.splits - 1) / a.splits);
   const int blk_lo = split * bps;
   const int blk_hi = min(nblk, blk_lo + bps);
-  const int nmine = blk_hi > blk_lo + warp ? (blk_hi - blk_lo - warp + W - 1) / W : 0;
+  const int nmine = blk_hi > blk_lo + warp ? (blk_hi - blk_lo - warp + kV3Warps - 1) / kV3Warps : 0;
 
   const int64_t tile = (int64_t)kBlk * D;
   const int64_t koff = (((int64_t)a.layer * 2 + 0) * a.kv_heads + kvh) * tile;
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(W * 32, W == 2 ? 4 : (S == 2 ? 3 : 2)) paged_a
 
   auto issue = [&](int j) {  // warp-local block j -> stage j % S
     if (j < nmine) {
-      const int blk = blk_lo + warp + j * W;
+      const int blk = blk_lo + warp + j * kV3Warps;
       const int64_t base = (int64_t)__ldg(trow + blk) * a.block_elems;
       uint16_t* ks = ring + (j % S) * 2 * kTileElems;
       uint16_t* vs = ks + kTileElems;
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(W * 32, W == 2 ? 4 : (S == 2 ? 3 : 2)) paged_a
     __syncwarp();
     const uint16_t* ks = ring + (j % S) * 2 * kTileElems;
     const uint16_t* vs = ks + kTileElems;
-    const int blk = blk_lo + warp + j * W;
+    const int blk = blk_lo + warp + j * kV3Warps;
     // ---- S = Q K^T : two n-tiles of 8 tokens, 8 k-steps of 16 dims
     float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row within matrix, matrix id
@@ -755,8 +755,8 @@ __global__ void __launch_bounds__(W * 32, W == 2 ? 4 : (S == 2 ? 3 : 2)) paged_a
 
   // ---- merge the 4 warps (reuse the ring memory), write split / output
   __syncthreads();
-  float* acc_sh = reinterpret_cast<float*>(smem_raw);  // [W][G][D]
-  __shared__ float m_sh[W][8], l_sh[W][8];
+  float* acc_sh = reinterpret_cast<float*>(smem_raw);  // [kV3Warps][G][D]
+  __shared__ float m_sh[kV3Warps][8], l_sh[kV3Warps][8];
   if (r0 < G) {
 #pragma unroll
     for (int n = 0; n < 16; ++n) {
@@ -773,10 +773,10 @@ __global__ void __launch_bounds__(W * 32, W == 2 ? 4 : (S == 2 ? 3 : 2)) paged_a
     const int g = e / D, d = e % D;
     float mm = -FLT_MAX;
 #pragma unroll
-    for (int w = 0; w < W; ++w) mm = fmaxf(mm, m_sh[w][g]);
+    for (int w = 0; w < kV3Warps; ++w) mm = fmaxf(mm, m_sh[w][g]);
     float ll = 0.f, aa = 0.f;
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
+    for (int w = 0; w < kV3Warps; ++w) {
       const float f = (m_sh[w][g] == -FLT_MAX) ? 0.f : exp2f(m_sh[w][g] - mm);
       ll += l_sh[w][g] * f;
       aa += acc_sh[(w * G + g) * D + d] * f;
@@ -1133,15 +1133,6 @@ static int attn_impl() {
   return impl;
 }
 
-static int v3_warps() {
-  static int w = -1;
-  if (w < 0) {
-    const char* e = getenv("TF_ATTN_WARPS");
-    w = (e && e[0] == '2') ? 2 : 4;
-  }
-  return w;
-}
-
 static int v3_stages() {
   static int st = -1;
   if (st < 0) {
@@ -1167,7 +1158,7 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
     minblk = m ? std::max(1, atoi(m)) : 8;
     g_minblk = minblk;
   }
-  const int per_sm = attn_impl() >= 3 ? (v3_warps() == 2 ? 4 : (v3_stages() == 2 ? 3 : 2)) : 2;  // resident CTAs/SM
+  const int per_sm = attn_impl() >= 3 ? (v3_stages() == 2 ? 3 : 2) : 2;  // resident CTAs per SM
   const int target = attn_impl() >= 2 ? 148 * per_sm * waves : 148 * 6;
   int s = std::max(1, std::min((target + base - 1) / base, (nblk + minblk - 1) / minblk));
   int per = (nblk + s - 1) / s;
@@ -1211,21 +1202,16 @@ static int launch(const AttnArgs& a, int B, cudaStream_t st) {
   if (attn_impl() >= 3 && D == 128 && G <= 8) {
     constexpr int GG = G <= 8 ? G : 8;
     const int S = v3_stages();
-    const int W = v3_warps();
-    const int smem = W * S * 2 * kBlk * kRowPad * 2;
+    const int smem = kV3Warps * S * 2 * kBlk * kRowPad * 2;
     static bool attr3 = false;
     if (!attr3) {
       TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kV3Warps * 2 * 2 * kBlk * kRowPad * 2));
       TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kV3Warps * 3 * 2 * kBlk * kRowPad * 2));
-      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   2 * 3 * 2 * kBlk * kRowPad * 2));
       attr3 = true;
     }
-    if (W == 2)
-      paged_attn_mma_kernel<GG, 3, 2><<<grid, 2 * 32, smem, st>>>(a);
-    else if (S == 2)
+    if (S == 2)
       paged_attn_mma_kernel<GG, 2><<<grid, kV3Warps * 32, smem, st>>>(a);
     else
       paged_attn_mma_kernel<GG, 3><<<grid, kV3Warps * 32, smem, st>>>(a);
