@@ -54,6 +54,9 @@ extern "C" {
 
 const char* tf_last_error(void);
 int tf_abi_version(void);
+/* Kernel launches issued through this library so far (captured launches
+ * count once, at capture - a graph replay re-runs them without calling in). */
+int64_t tf_launch_count(void);
 
 /* ------------------------------------------------------------------ pool --
  * Block-major KV layout shared by HBM pool and pinned host store:

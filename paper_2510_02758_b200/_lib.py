@@ -118,6 +118,7 @@ SIGNATURES = {
     "tf_kv_gather_d2h": (C.c_int, [_I64, C.POINTER(TfSeg), _I32, _I32, _I32, _I32, _P]),
     "tf_kv_scatter_h2d": (C.c_int, [_I64, C.POINTER(TfSeg), _I32, _I32, _I32, _I32, _P]),
     "tf_copy_small": (C.c_int, [_P, _P, _I64, _P]),
+    "tf_launch_count": (_I64, []),
     "tf_rmsnorm": (C.c_int, [_P, _P, _P, _I32, _I32, C.c_float, _P]),
     "tf_silu_mul": (C.c_int, [_P, _P, _I32, _I32, _P]),
     "tf_kv_append": (C.c_int, [_I64, _P, _I32, _P, _P, _I32, _I32, _P, _P, _I64, _P]),

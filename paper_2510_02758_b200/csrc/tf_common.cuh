@@ -32,8 +32,12 @@ void set_error(const char* fmt, ...);
     }                                                                                          \
   } while (0)
 
+// every kernel launch of the library passes here: counted for tf_launch_count()
+void count_launch();
+
 #define TF_LAUNCH_CHECK()                                                                       \
   do {                                                                                          \
+    ::tf::count_launch();                                                                       \
     cudaError_t _e = cudaGetLastError();                                                        \
     if (_e != cudaSuccess) {                                                                    \
       ::tf::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), __FILE__, __LINE__); \

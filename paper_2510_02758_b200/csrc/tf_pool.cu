@@ -10,11 +10,16 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <atomic>
+
 #include "tf_common.cuh"
 
 namespace tf {
 
 static thread_local char g_err[1024] = "";
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -58,6 +63,8 @@ using namespace tf;
 extern "C" {
 
 const char* tf_last_error(void) { return g_err; }
+
+int64_t tf_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 int tf_abi_version(void) { return 1; }
 
 double tf_host_glibc_exp(double x);

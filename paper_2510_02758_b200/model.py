@@ -115,6 +115,13 @@ class PagedDecoder:
             self._dec_out = torch.zeros(4096, dtype=torch.long, pin_memory=True)  # sampled ids readback
         self._graphs = {}
         self._pgraphs = {}  # recompute prefill graphs per token bucket
+        self._graph_launches = {}  # this library's kernels captured per graph
+        self.replayed_launches = 0  # ... and re-run by graph replays so far
+
+    def launch_count(self) -> int:
+        """This library's kernel launches so far: direct C-ABI launches plus
+        the captured ones every graph replay re-ran."""
+        return int(lib.tf_launch_count()) + self.replayed_launches
 
     # ------------------------------------------------------------ pieces
     def prompt_tokens(self, rid: int, n: int) -> torch.Tensor:
@@ -372,8 +379,10 @@ class PagedDecoder:
                 self._forward_graphable(dp, io, Bp, ws, st)  # warm-up (kernel attributes, cuBLAS handles)
             st.synchronize()
             g = torch.cuda.CUDAGraph()
+            c0 = lib.tf_launch_count()
             with torch.cuda.graph(g, pool=mempool, stream=st):
                 out = self._forward_graphable(dp, io, Bp, ws, torch.cuda.current_stream())
+            self._graph_launches[("decode", Bp)] = lib.tf_launch_count() - c0
             self._graphs[Bp] = (g, io, stage, out, ws)
         st.synchronize()
         if prefill_buckets:
@@ -400,8 +409,10 @@ class PagedDecoder:
                 self._prefill_core(dp, tok, rows, pos32, cu, T, last, st)  # warm-up
             st.synchronize()
             g = torch.cuda.CUDAGraph()
+            c0 = lib.tf_launch_count()
             with torch.cuda.graph(g, pool=mempool, stream=st):
                 self._prefill_core(dp, tok, rows, pos32, cu, T, last, torch.cuda.current_stream())
+            self._graph_launches[("recompute", T)] = lib.tf_launch_count() - c0
             stage_tok = torch.zeros(T, dtype=torch.int64, pin_memory=True)
             stage_meta = torch.zeros(2 * T + 3, dtype=torch.int32, pin_memory=True)
             self._pgraphs[T] = (g, tok, meta, last, stage_tok, stage_meta)
@@ -426,6 +437,7 @@ class PagedDecoder:
                                         dst.numel() * dst.element_size(), C.c_void_p(st.cuda_stream)),
                       "tf_copy_small")
             g.replay()
+            self.replayed_launches += self._graph_launches.get(("recompute", T), 0)
 
     def _forward_graphable(self, dp, io, Bp, ws, st):
         rows = io[1].to(torch.int32)
@@ -454,6 +466,7 @@ class PagedDecoder:
             if tokens_dev is not None:
                 io[0, :B].copy_(tokens_dev)
             g.replay()
+            self.replayed_launches += self._graph_launches.get(("decode", Bp), 0)
         # the staging buffer is reused next step only after this step completed
         return out[:B]
 
