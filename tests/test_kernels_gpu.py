@@ -226,3 +226,18 @@ def test_silu_mul_vs_torch(cuda, rows, ffn):
     g, u = gu.float().chunk(2, dim=-1)
     ref = F.silu(g) * u
     assert ((y.float() - ref).abs() <= 2 ** -6 * ref.abs() + 1e-3).all()
+
+
+def test_launch_counter_counts_library_kernels(cuda):
+    """tf_launch_count (the bench's gpu_launches) advances by one per kernel
+    the library launches."""
+    lib = _lib()
+    x = torch.randn(4, 256, device=cuda).to(torch.bfloat16)
+    w = torch.ones(256, device=cuda).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    c0 = lib.lib.tf_launch_count()
+    for _ in range(3):
+        lib.check(lib.lib.tf_rmsnorm(C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr()),
+                                     4, 256, 1e-5, None))
+    torch.cuda.synchronize()
+    assert lib.lib.tf_launch_count() - c0 == 3
