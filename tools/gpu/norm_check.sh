@@ -1,0 +1,18 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_kernels_gpu.py tests/test_realtime_gpu.py tests/test_tp_gpu.py -m gpu -q > gpurun_out/pytest_norm.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_norm.log
+python - > gpurun_out/norm_time.log 2>&1 <<'PY'
+import sys, ctypes as C, torch
+sys.path.insert(0, '.')
+from paper_2510_02758_b200 import _lib
+x = torch.randn(128, 4096, device='cuda').to(torch.bfloat16); w = torch.ones(4096, device='cuda').to(torch.bfloat16); y = torch.empty_like(x)
+def f(): _lib.check(_lib.lib.tf_rmsnorm(C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr()), 128, 4096, 1e-5, None))
+for _ in range(10): f()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    for _ in range(100): f()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+print("rmsnorm B=128 D=4096 per launch (graph): %.2f us" % (e0.elapsed_time(e1) * 10))
+PY
+cat gpurun_out/norm_time.log; tail -n 2 gpurun_out/pytest_norm.log
