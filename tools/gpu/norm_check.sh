@@ -1,11 +1,11 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_kernels_gpu.py tests/test_realtime_gpu.py tests/test_tp_gpu.py -m gpu -q > gpurun_out/pytest_norm.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_norm.log
+true
 python - > gpurun_out/norm_time.log 2>&1 <<'PY'
 import sys, ctypes as C, torch
 sys.path.insert(0, '.')
 from paper_2510_02758_b200 import _lib
 x = torch.randn(128, 4096, device='cuda').to(torch.bfloat16); w = torch.ones(4096, device='cuda').to(torch.bfloat16); y = torch.empty_like(x)
-def f(): _lib.check(_lib.lib.tf_rmsnorm(C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr()), 128, 4096, 1e-5, None))
+def f(): _lib.check(_lib.lib.tf_rmsnorm(C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr()), 128, 4096, 1e-5, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 for _ in range(10): f()
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g):
