@@ -3,8 +3,8 @@
 // generic layer-norm and two-pass silu/mul kernels cost ~17% of a C2 decode
 // step (profiles/r1_bench_window_launches.txt), so these replace them:
 //
-//   tf_rmsnorm     y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w   (one warp per row,
-//                  all 16-B loads of the row in flight, fp32 sum, shuffle reduce)
+//   tf_rmsnorm     y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w   (one CTA per row,
+//                  16-B vector loads, fp32 sum, row held in registers)
 //   tf_silu_mul    y = silu(gu[:, :F]) * gu[:, F:]                (one pass, 16-B vectors)
 #include <algorithm>
 
@@ -30,49 +30,45 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-constexpr int kNormWarps = 4;   // rows per CTA: one warp per row (no block-wide barrier)
-constexpr int kNormMaxVec = 32;  // 16-B vectors per lane held in registers: D <= 32*32*8 = 8192
+constexpr int kNormThreads = 256;
+constexpr int kNormMaxVec = 4;  // 16-B vectors per thread held in registers: D <= 256*4*8 = 8192
 
-__global__ void __launch_bounds__(kNormWarps * 32) rmsnorm_kernel(const uint16_t* __restrict__ x,
-                                                                const uint16_t* __restrict__ w,
-                                                                uint16_t* __restrict__ y, int rows, int D,
-                                                                float eps) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * kNormWarps + (threadIdx.x >> 5);
-  if (row >= rows) return;
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* __restrict__ x,
+                                                             const uint16_t* __restrict__ w,
+                                                             uint16_t* __restrict__ y, int D, float eps) {
+  const int64_t row = blockIdx.x;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * D);
   const uint4* wr = reinterpret_cast<const uint4*>(w);
   uint4* yr = reinterpret_cast<uint4*>(y + row * D);
   const int nv = D / 8;
-  uint4 raw[kNormMaxVec];
-#pragma unroll
-  for (int k = 0; k < kNormMaxVec; ++k) {  // every load of the row in flight at once
-    const int i = lane + k * 32;
-    if (i < nv) raw[k] = xr[i];
-  }
+  float v[kNormMaxVec][8];
   float ss = 0.f;
 #pragma unroll
   for (int k = 0; k < kNormMaxVec; ++k) {
-    const int i = lane + k * 32;
+    const int i = threadIdx.x + k * kNormThreads;
     if (i < nv) {
-      float v[8];
-      unpack8(raw[k], v);
+      unpack8(xr[i], v[k]);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) ss += v[e] * v[e];
+      for (int e = 0; e < 8; ++e) ss += v[k][e] * v[k][e];
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const float r = rsqrtf(ss / (float)D + eps);
+  __shared__ float part[kNormThreads / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < kNormThreads / 32; ++i) tot += part[i];
+  const float r = rsqrtf(tot / (float)D + eps);
 #pragma unroll
   for (int k = 0; k < kNormMaxVec; ++k) {
-    const int i = lane + k * 32;
+    const int i = threadIdx.x + k * kNormThreads;
     if (i < nv) {
-      float v[8], g[8], o[8];
-      unpack8(raw[k], v);
+      float g[8], o[8];
       unpack8(__ldg(wr + i), g);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(v[e] * r)) * g[e];
+      for (int e = 0; e < 8; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(v[k][e] * r)) * g[e];
       yr[i] = pack8(o);
     }
   }
@@ -106,12 +102,12 @@ using namespace tf;
 extern "C" {
 
 int tf_rmsnorm(const void* x, const void* w, void* y, int32_t rows, int32_t dim, float eps, void* stream) {
-  TF_CHECK_ARG(rows >= 0 && dim > 0 && dim % 8 == 0 && dim <= 32 * kNormMaxVec * 8,
+  TF_CHECK_ARG(rows >= 0 && dim > 0 && dim % 8 == 0 && dim <= kNormThreads * kNormMaxVec * 8,
                "tf_rmsnorm: bad shape %d x %d", rows, dim);
   if (rows == 0) return TF_OK;
   TF_CHECK_ARG(x && w && y, "tf_rmsnorm: NULL pointer");
-  rmsnorm_kernel<<<(rows + kNormWarps - 1) / kNormWarps, kNormWarps * 32, 0, (cudaStream_t)stream>>>(
-      (const uint16_t*)x, (const uint16_t*)w, (uint16_t*)y, rows, dim, eps);
+  rmsnorm_kernel<<<rows, kNormThreads, 0, (cudaStream_t)stream>>>((const uint16_t*)x, (const uint16_t*)w,
+                                                                  (uint16_t*)y, dim, eps);
   TF_LAUNCH_CHECK();
   return TF_OK;
 }
