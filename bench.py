@@ -201,6 +201,9 @@ def run_ours(args):
             tp_before, mode_before = dict(policy._t_prime), policy.mode
             dec = orig_tick(view)
             if lo_t <= view.now <= hi_t:
+                # a device-built snapshot (RowsSnapshot) is dumped as its host
+                # equivalent, so the shadow check also verifies the builder
+                view = view.materialize() if getattr(view, "materialize", None) else view
                 snap = {k: getattr(view, k) for k in ("now", "free_slots", "gpu_mem_free", "gpu_mem_total",
                                                       "cpu_mem_total", "max_batch", "gamma", "prefill_s_per_token",
                                                       "offload_enabled", "h2d_blocked_tokens")}
