@@ -140,3 +140,33 @@ def test_pysum_matches_builtin_sum():
               for _ in range(rng.randint(0, 10))]
         a, b = sum(xs), pysum(xs)
         assert a == b and math.copysign(1, a) == math.copysign(1, b)
+
+
+def test_realtime_b200_ticks_match_oracle():
+    """Every on_tick decision the GPU selector took during a real-time C2 bench
+    run on a B200 (member view built on the device; recorded by
+    ``bench.py --dump-ticks``) equals the oracle restatement's decision on the
+    same snapshot and policy state - parity in the measured regime, not only on
+    the reference's own recorded ticks."""
+    import gzip
+    import json
+    from dataclasses import asdict
+
+    from conftest import GOLDEN
+
+    from oracle.refsim.policy import Knobs, TokenFlowPolicy, snapshot_from_dict
+    from paper_2510_02758_b200 import configs
+    from paper_2510_02758_b200.scheduler import SchedulerConfig
+
+    d = json.load(gzip.open(GOLDEN / "realtime" / "c2_burst_b200_ticks.json.gz"))
+    knobs = Knobs(**asdict(configs.C2.sched_cfg(SchedulerConfig)))
+    assert len(d["ticks"]) > 100
+    for t in d["ticks"]:
+        pol = TokenFlowPolicy(knobs)
+        pol._t_prime = {int(k): v for k, v in t["t_prime"]}
+        pol.mode = t["mode_before"]
+        want = pol.on_tick(snapshot_from_dict(t["snapshot"]))
+        assert (want.mode, list(want.preempt), [list(r) for r in want.resume],
+                [list(b) for b in want.prefill_batches]) == \
+            (t["mode"], t["preempt"], [list(r) for r in t["resume"]], t["prefill_batches"])
+        assert sorted((int(k), v) for k, v in pol._t_prime.items()) == [(int(k), v) for k, v in t["t_prime_after"]]
