@@ -1,27 +1,35 @@
 """Benchmark: effective tok/s (+ P99 TTFT, KV swap GB/s) of the B200 TokenFlow
-hot path on C2 (Llama3-8B bf16 random-init, 256-request Poisson trace with
-KV swap to pinned host), 1 GPU per process.
+hot path on C2 (Llama3-8B bf16 random-init, the 256-request C2 population
+arriving as a burst at t=0, KV swap to pinned host), 1 GPU per process.
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--full-run]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                [--config c2|c4] [--arrivals burst|poisson] [--full-run]
 
 A *step* is one decode iteration of the real-time serving loop
-(realtime.RealtimeEngine) in its contended regime: the GPU selector's
-pacing/tick decisions, the Llama3-8B forward with paged KV append + paged
-decode attention for the batch, and the write-through / evict / load chunks
-the engine issues meanwhile on the two copy streams.  The loop first runs
-untimed from t=0 until requests are being preempted and swapped (contention),
-then W warm-up steps, then EXACTLY K timed steps.
+(realtime.RealtimeEngine): the GPU selector's pacing / tick decisions (member
+view built on the device), the Llama3-8B forward (captured CUDA graph: fused
+RMSNorm / rope+append / paged attention / SwiGLU around cuBLAS GEMMs) and the
+write-through / evict / load chunks the engine issues meanwhile on the two
+high-priority copy streams.  W warm-up steps from t=0, then EXACTLY K timed
+steps (default 1000: the admission / preemption / swap-heavy phase of the
+burst).
 
 value  = effective tokens (tokensim.metrics weights, tau1/tau2 = 10%/20% of
-         the output length) generated in the K steps / device time of those
-         K decode iterations (CUDA events on the compute stream), max over
-         ranks; inputs (weights, KV) already resident in HBM.
+         the output length) generated in the K steps / device time of every
+         GPU job (decode steps and the prefills between them) in the window
+         (CUDA events on the compute stream), max over ranks; weights and KV
+         resident in HBM.
 e2e    = the same tokens / host wall-clock span of the K steps through the
-         public API (engine loop), which includes every step's H2D (token
-         ids, positions, block-table deltas, load chunks) and D2H (sampled
-         token ids, evict / write-through chunks).
-The working set (16 GB weights + ~20 GiB KV per step) exceeds the 126 MB L2
-(no flush needed).  Multi-GPU: request i -> replica i mod N (C3), weak scaling.
+         public API (engine loop), including every step's host<->device
+         traffic (step inputs, sampled ids, load / write-through / evict
+         chunks: h2d_bytes_per_step / d2h_bytes_per_step).
+ttft   = after the window the loop keeps serving until every request of the
+         burst has its first token: complete nearest-rank P99 TTFT.
+roofline / swap.hidden_under_decode are measured right after the window on
+the running batch; gpu_launches are counted by the library.  The working set
+(16 GB weights + ~20 GiB KV) exceeds the 126 MB L2 (no flush needed).
+Multi-GPU: request i -> replica i mod N (C3, weak scaling); --config c4 runs
+Qwen2.5-32B tensor-parallel over the launched ranks (strong scaling).
 """
 from __future__ import annotations
 
