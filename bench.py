@@ -155,6 +155,11 @@ def run_ours(args):
     from paper_2510_02758_b200.scheduler import BufferAwarePolicy, SchedulerConfig
 
     world, rank, local = _dist()
+    # (debug: TF_BENCH_ONE_GPU=1 runs every rank on cuda:0 with a gloo group,
+    # to exercise the multi-rank code path on a one-GPU box)
+    one_gpu = os.environ.get("TF_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     tp_mode = args.config == "c4"
@@ -162,7 +167,10 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     if tp_mode:
         # C4: one model over all ranks (TP = world), NCCL all-reduces on the
         # data path, completion/clock consensus over a CPU group on the control path
