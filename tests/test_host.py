@@ -172,3 +172,20 @@ def test_library_host_entry_points():
     with pytest.raises(ValueError):
         check(lib.tf_pool_init(C.c_void_p(256), 8, None, 0, 2, 16, 2, 60, 0, C.byref(h)))
     check(lib.tf_pool_destroy(h))
+
+
+def test_bench_helpers():
+    """bench.py's roofline traffic (scaled from the committed ncu capture) and
+    TTFT summary (nearest-rank P99 over first-token latencies)."""
+    import types
+
+    import bench
+
+    t, src = bench._ncu_traffic(400e6)
+    assert src and "ncu" in src and 1.0 <= t / 400e6 <= 1.1
+    recs = [types.SimpleNamespace(gen_times=[float(i) + 1.0], arrival=0.0) for i in range(100)]
+    s = bench._ttft_summary(recs, 100, 1, False)
+    v = [float(i) + 1.0 for i in range(100)]
+    assert s["complete"] and s["requests"] == 100
+    assert s["p99_s"] == metrics.nearest_rank(v, 99.0) and s["p50_s"] == metrics.nearest_rank(v, 50.0)
+    assert bench._ttft_summary([], 5, 1, False) is None
