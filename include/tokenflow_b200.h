@@ -231,7 +231,10 @@ typedef struct {
 } tf_tick_params;
 
 /* On-device snapshot builder input: the engine's raw
- * per-request counters, ALL requests in request-id order; the device derives
+ * per-request counters in request-id order (the engine packs only requests
+ * in service and not generation-complete; rows of other requests are
+ * accepted and skipped; n_rows <= the selector's max_members <= 1024, the
+ * concurrent-member capacity of the single-CTA kernels); the device derives
  * the MemberView rows of tokensim/engine.py:993-1061 (membership = in service
  * and not generation-complete; t_io = io_overhead_estimate, kvstore.py:173-193;
  * t_recompute = prefill_s_per_token * total_kv) in the reference's operation

@@ -55,6 +55,7 @@ struct Pool {
   int64_t block_elems;  // elements per block (all layers)
   int64_t tile_elems;   // block_tokens * head_dim (one (block,layer,kv,head) tile)
   std::vector<int32_t> free_gpu, free_host;  // LIFO stacks (back = next)
+  std::vector<uint8_t> used_gpu, used_host;  // per-block allocation state (double-free check)
 
   // element offset of (block, layer, kv, head, slot, dim=0)
   __host__ __device__ int64_t off(int64_t b, int l, int kv, int h, int s) const {

@@ -104,6 +104,8 @@ int tf_pool_init(void* gpu_pool, int32_t n_blocks, void* host_pool, int32_t n_ho
   for (int32_t i = 0; i < n_blocks; ++i) p->free_gpu[i] = n_blocks - 1 - i;
   p->free_host.resize(n_host_blocks);
   for (int32_t i = 0; i < n_host_blocks; ++i) p->free_host[i] = n_host_blocks - 1 - i;
+  p->used_gpu.assign(n_blocks, 0);
+  p->used_host.assign(n_host_blocks, 0);
   std::lock_guard<std::mutex> lk(g_mu);
   int64_t h = g_next++;
   g_pools[h] = std::move(p);
@@ -128,12 +130,14 @@ int tf_blocks_alloc(int64_t pool, int32_t tier, int32_t n, int32_t* out_ids) {
   TF_CHECK_ARG(tier == TF_TIER_GPU || tier == TF_TIER_HOST, "tf_blocks_alloc: bad tier %d", tier);
   TF_CHECK_ARG(n >= 0 && (n == 0 || out_ids), "tf_blocks_alloc: bad n/out");
   auto& st = tier == TF_TIER_GPU ? p->free_gpu : p->free_host;
+  auto& used = tier == TF_TIER_GPU ? p->used_gpu : p->used_host;
   if ((int64_t)st.size() < n) {
     set_error("tf_blocks_alloc: %s tier exhausted (%d requested, %zu free)", tier ? "host" : "gpu", n, st.size());
     return TF_ENOMEM;
   }
   for (int32_t i = 0; i < n; ++i) {
     out_ids[i] = st.back();
+    used[st.back()] = 1;
     st.pop_back();
   }
   return TF_OK;
@@ -143,13 +147,29 @@ int tf_blocks_free(int64_t pool, int32_t tier, const int32_t* ids, int32_t n) {
   Pool* p = get_pool(pool);
   TF_CHECK_ARG(p, "tf_blocks_free: unknown pool");
   TF_CHECK_ARG(tier == TF_TIER_GPU || tier == TF_TIER_HOST, "tf_blocks_free: bad tier %d", tier);
+  TF_CHECK_ARG(n >= 0 && (n == 0 || ids), "tf_blocks_free: bad n/ids");
   auto& st = tier == TF_TIER_GPU ? p->free_gpu : p->free_host;
+  auto& used = tier == TF_TIER_GPU ? p->used_gpu : p->used_host;
   int32_t cap = tier == TF_TIER_GPU ? p->n_blocks : p->n_host_blocks;
+  // validate the whole list before touching the stack: a rejected call leaves
+  // the allocator unchanged (no partial push); state 2 marks "listed in this
+  // call" so a duplicate id inside the list is caught as well
   for (int32_t i = 0; i < n; ++i) {
-    TF_CHECK_ARG(ids[i] >= 0 && ids[i] < cap, "tf_blocks_free: block %d out of range", ids[i]);
+    const bool in_range = ids[i] >= 0 && ids[i] < cap;
+    if (!in_range || used[ids[i]] != 1) {
+      for (int32_t k = 0; k < i; ++k) used[ids[k]] = 1;
+      if (!in_range)
+        set_error("tf_blocks_free: block %d out of range", ids[i]);
+      else
+        set_error("tf_blocks_free: double free of block %d", ids[i]);
+      return TF_EINVAL;
+    }
+    used[ids[i]] = 2;
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    used[ids[i]] = 0;
     st.push_back(ids[i]);
   }
-  TF_CHECK_ARG((int64_t)st.size() <= cap, "tf_blocks_free: double free (stack exceeds capacity)");
   return TF_OK;
 }
 

@@ -543,19 +543,22 @@ class GpuDataPlane:
         n_layers = self.pool.L if self.attention == "all" else int(self.attention)
         st = self.s_compute
         B = len(batch)
-        rows = torch.tensor(list(batch), dtype=torch.int32).pin_memory().to(self.pool.device, non_blocking=True)
         pos = [eng.state[r].kv.total_kv for r in batch]
-        ctx = torch.tensor([p + 1 for p in pos], dtype=torch.int32).pin_memory().to(self.pool.device,
-                                                                                      non_blocking=True)
-        posd = torch.tensor(pos, dtype=torch.int32).pin_memory().to(self.pool.device, non_blocking=True)
         hq = self.n_q_heads
-        q = torch.empty((B, hq, self.pool.D), dtype=torch.int16, device=self.pool.device)
-        out = torch.empty_like(q)
-        ws_need = int(lib.tf_paged_decode_attn_workspace(self.pool.handle, B, max(pos) + 1, hq))
-        if ws_need > self._attn_ws.numel():
-            self._attn_ws = torch.zeros(ws_need, dtype=torch.uint8, device=self.pool.device)
         scale = 1.0 / float(self.pool.D) ** 0.5
+        # every input is uploaded / allocated ON the launching stream: the
+        # kernels are stream-ordered after their copies, and the caching
+        # allocator only recycles these blocks once st has passed them
         with torch.cuda.stream(st):
+            rows = torch.tensor(list(batch), dtype=torch.int32).pin_memory().to(self.pool.device, non_blocking=True)
+            ctx = torch.tensor([p + 1 for p in pos], dtype=torch.int32).pin_memory().to(self.pool.device,
+                                                                                          non_blocking=True)
+            posd = torch.tensor(pos, dtype=torch.int32).pin_memory().to(self.pool.device, non_blocking=True)
+            q = torch.empty((B, hq, self.pool.D), dtype=torch.int16, device=self.pool.device)
+            out = torch.empty_like(q)
+            ws_need = int(lib.tf_paged_decode_attn_workspace(self.pool.handle, B, max(pos) + 1, hq))
+            if ws_need > self._attn_ws.numel():
+                self._attn_ws = torch.zeros(ws_need, dtype=torch.uint8, device=self.pool.device)
             for layer in range(n_layers):
                 check(lib.tf_q_fill_synthetic(C.c_void_p(q.data_ptr()), C.c_void_p(rows.data_ptr()),
                                               C.c_void_p(posd.data_ptr()), B, layer, hq, self.pool.D, self.seed,

@@ -16,7 +16,7 @@ wall clock and every duration comes from the hardware:
 ``lockstep`` (tensor parallelism, C4): every TP rank runs this same engine
 on its own shard; completions are agreed with one small collective per
 loop iteration (``Lockstep.agree``: a completion counts once it fired on
-EVERY rank, at the LATEST rank's time; the clock is the latest rank's), so
+EVERY rank, at the LATEST rank's time; the clock is the earliest rank's), so
 all ranks see the same event sequence at the same times and the
 deterministic engine + bit-exact selector take identical decisions with no
 decision broadcast.
@@ -164,6 +164,10 @@ class RealtimeEngine(Engine):
         Lockstep: done flags, end and start times and the clock are agreed
         over the TP ranks."""
         slots = (("gpu", self._gpu, 0), ("d2h", self._lanes["d2h"], 1), ("h2d", self._lanes["h2d"], 1))
+        # the clock is read BEFORE the events are queried: a job not observed
+        # done below finishes after `clock`, so draining the heap up to `clock`
+        # can never run an event that a still-unobserved completion precedes
+        clock = self._clock()
         flags, ends, starts = [], [], []
         for what, v, _ in slots:
             # v = (host start time, end event, start event)
@@ -177,7 +181,6 @@ class RealtimeEngine(Engine):
             else:
                 starts.append(0.0)
                 ends.append(0.0)
-        clock = self._clock()
         if self.lockstep is not None:
             clock, flags, ends, starts = self.lockstep.agree(clock, flags, ends, starts)
         done = [(t, order, what, s0) for (what, _, order), ok, t, s0 in zip(slots, flags, ends, starts) if ok]

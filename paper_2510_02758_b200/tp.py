@@ -15,7 +15,7 @@ Two collectives, nothing else:
   broadcasting rank 0's decisions, every rank runs the same deterministic
   engine and bit-exact GPU selector on the same agreed event sequence: a
   completion (decode step, prefill, d2h / h2d chunk) is taken once it fired on
-  every rank, at the latest rank's device time, and the clock is the latest
+  every rank, at the latest rank's device time, and the clock is the earliest
   rank's.  Identical inputs -> identical decisions, block tables and chunk
   sequences on every rank (checked at the end with ``Lockstep.same``).
 """
@@ -39,10 +39,14 @@ class Lockstep:
 
     def agree(self, clock: float, flags, ends, starts):
         """-> (clock, flags, ends, starts) agreed over the ranks: an item is
-        done iff done on every rank; its end / start is the latest rank's."""
+        done iff done on every rank; its end / start is the latest rank's; the
+        clock is the EARLIEST rank's (each rank read it before querying its
+        events, so an item not yet done on some rank ends after that rank's
+        clock, hence after the agreed one - events up to the agreed clock can
+        be drained before any completion still to come)."""
         k = len(flags)
         v = np.empty(1 + 3 * k, dtype=np.float64)
-        v[0] = clock
+        v[0] = -clock  # max of -clock = min clock
         for i in range(k):
             # max-reduction of (1 - done): an item is done only if done everywhere
             v[1 + i] = 0.0 if flags[i] else 1.0
@@ -51,7 +55,7 @@ class Lockstep:
         t = torch.from_numpy(v)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         self.calls += 1
-        return (float(v[0]), [v[1 + i] == 0.0 for i in range(k)], [float(v[1 + k + i]) for i in range(k)],
+        return (-float(v[0]), [v[1 + i] == 0.0 for i in range(k)], [float(v[1 + k + i]) for i in range(k)],
                 [float(v[1 + 2 * k + i]) for i in range(k)])
 
     def same(self, text: str) -> bool:

@@ -137,6 +137,13 @@ def test_metric_known_answers():
     assert metrics.effective_token_weight(20, 100, cfg) == 0.0
     assert metrics.nearest_rank([1.0, 2.0, 3.0], 99.0) == 3.0
     assert metrics.replay_rebuffer(0.0, [0.0, 0.05, 0.5], 20.0) == pytest.approx(0.4)
+    # QosConfig validates like tokensim/metrics.py:25-31
+    for bad in ({"buffer_threshold_frac": 0.0}, {"buffer_threshold_frac": 1.0}, {"decay_alpha": 0.0},
+                {"ttft_penalty_weight": -1.0}, {"rebuffer_penalty_weight": -0.5}):
+        with pytest.raises(metrics.MetricError):
+            metrics.QosConfig(**bad)
+    with pytest.raises(metrics.MetricError):
+        scheduler.SchedulerConfig(value_threshold_frac=1.5).value_config()
 
 
 def test_library_exports_every_header_symbol():
@@ -167,6 +174,18 @@ def test_library_host_entry_points():
     again = (C.c_int32 * 1)()
     check(lib.tf_blocks_alloc(h, 0, 1, again))
     assert again[0] == 2  # LIFO: the last freed block is handed out first
+    # double free below capacity, a duplicate inside one list and an
+    # out-of-range id are all rejected without changing the allocator
+    n_free = lib.tf_blocks_free_count(h, 0)
+    with pytest.raises(ValueError, match="double free"):
+        check(lib.tf_blocks_free(h, 0, (C.c_int32 * 1)(0), 1))
+    with pytest.raises(ValueError, match="double free"):
+        check(lib.tf_blocks_free(h, 0, (C.c_int32 * 2)(2, 2), 2))
+    with pytest.raises(ValueError, match="out of range"):
+        check(lib.tf_blocks_free(h, 0, (C.c_int32 * 2)(2, 99), 2))
+    assert lib.tf_blocks_free_count(h, 0) == n_free
+    check(lib.tf_blocks_free(h, 0, again, 1))  # block 2 is still allocated: a valid free
+    assert lib.tf_blocks_free_count(h, 0) == n_free + 1
     with pytest.raises(MemoryError):
         check(lib.tf_blocks_alloc(h, 0, 99, (C.c_int32 * 99)()))
     with pytest.raises(ValueError):
