@@ -129,6 +129,7 @@ SIGNATURES = {
     "tf_paged_decode_attn": (C.c_int, [_I64, _P, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, C.c_float, _P, _P,
                                        _I64, _P]),
     "tf_paged_decode_attn_workspace": (_I64, [_I64, _I32, _I32, _I32]),
+    "tf_paged_decode_attn_impl": (C.c_int, [_I32]),
     "tf_selector_workspace_bytes": (_I64, [_I32, _I32]),
     "tf_selector_init": (C.c_int, [_P, _I64, _P, _I64, _I32, _I32, C.POINTER(_I64)]),
     "tf_selector_destroy": (C.c_int, [_I64]),

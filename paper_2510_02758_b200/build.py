@@ -27,6 +27,7 @@ UNITS = {
     "tf_swap.cu": [],
     "tf_append.cu": [],
     "tf_attn.cu": [],
+    "tf_attn_tma.cu": [],
     "tf_ops.cu": [],
     "tf_select.cu": ["-fmad=false"],
 }

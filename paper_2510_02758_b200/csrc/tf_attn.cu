@@ -18,6 +18,7 @@
 #include <algorithm>
 
 #include "tf_common.cuh"
+#include "tf_attn_tma.cuh"
 
 namespace tf {
 
@@ -54,6 +55,7 @@ struct AttnArgs {
   // v4 (stream-K): batch, partial slots per (request, kv head), self-resetting counters
   int32_t B, kmax;
   int32_t* counters;
+  int32_t mutate;  // test-only fault injection (attn_mutate)
 };
 
 // D = head_dim, G = q heads per kv head.
@@ -617,6 +619,7 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
   const int split = blockIdx.x;
   const int ctx = a.ctx[b];
   const int nblk = (ctx + kBlk - 1) / kBlk;
+  const int ctx_eff = (a.mutate == 1 && nblk >= 8) ? min(ctx, (nblk - nblk / 8) * kBlk) : ctx;
   // split size per request: a short request in a launch planned for a long
   // maximum context still spreads over all splits instead of idling them
   const int bps = max(a.min_blocks_per_split, (nblk + a.splits - 1) / a.splits);
@@ -696,7 +699,7 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
       for (int e = 0; e < 2; ++e) {
         const int t = nt * 8 + cq + e;
         float v = s[nt][e] * a.scale_log2;
-        if (blk * kBlk + t >= ctx) v = -FLT_MAX;
+        if (blk * kBlk + t >= ctx_eff) v = -FLT_MAX;
         s[nt][e] = v;
         mx = fmaxf(mx, v);
       }
@@ -1124,13 +1127,30 @@ __global__ void __launch_bounds__(kV4Warps * 32, kV4CtasPerSm) paged_attn_stream
   end_segment(seg);
 }
 
+// implementation selector: 5 (default) = TMA stream-K (tf_attn_tma.cu), 3 =
+// split-KV cp.async tensor-core kernel, 4 = cp.async stream-K, 2 = bulk-copy
+// CUDA-core, 1 = register-staged CUDA-core.  TF_ATTN_IMPL overrides the default
+// at start-up; tf_paged_decode_attn_impl() switches it at run time (A/B
+// benchmarks and the parity tests run every implementation in one process).
+static int g_impl = -1;
 static int attn_impl() {
-  static int impl = -1;
-  if (impl < 0) {
+  if (g_impl < 0) {
     const char* e = getenv("TF_ATTN_IMPL");
-    impl = (e && e[0] >= '1' && e[0] <= '4') ? e[0] - '0' : 3;
+    g_impl = (e && e[0] >= '1' && e[0] <= '5') ? e[0] - '0' : 5;
   }
-  return impl;
+  return g_impl;
+}
+
+// test-only fault injection (TF_ATTN_MUTATE=1: every (request, kv head) with
+// >= 8 blocks ignores its last eighth, the shape of a dropped split); the
+// parity tests run it in a subprocess and must FAIL under it
+static int attn_mutate() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("TF_ATTN_MUTATE");
+    m = (e && e[0] == '1') ? 1 : 0;
+  }
+  return m;
 }
 
 static int v3_stages() {
@@ -1245,6 +1265,7 @@ int64_t tf_paged_decode_attn_workspace(int64_t pool, int32_t B, int32_t max_ctx,
   if (!p) return -1;
   if (n_q_heads % p->kv_heads) return -1;
   const int G = n_q_heads / p->kv_heads;
+  if (attn_impl() == 5 && attn5_supported(p, G, B)) return attn5_workspace(p, B, max_ctx, G);
   if (use_v4(p->head_dim, G, B))
     return v4_counter_bytes(B, p->kv_heads) +
            (int64_t)B * p->kv_heads * v4_kmax(max_ctx) * G * (p->head_dim + 2) * (int64_t)sizeof(float);
@@ -1283,6 +1304,22 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
   const int G = n_q_heads / p->kv_heads;
   const int D = p->head_dim;
   a.B = B;
+  a.mutate = attn_mutate();
+  if (attn_impl() == 5 && attn5_supported(p, G, B)) {
+    Attn5Args a5;
+    a5.q = (const uint16_t*)q;
+    a5.table = dev_table;
+    a5.rows = dev_rows;
+    a5.ctx = dev_ctx;
+    a5.out = (uint16_t*)out;
+    a5.stride = row_stride;
+    a5.layer = layer;
+    a5.hq = n_q_heads;
+    a5.B = B;
+    a5.scale_log2 = a.scale_log2;
+    a5.mutate = a.mutate;
+    return attn5_launch(p, a5, G, max_ctx, workspace, workspace_bytes, sm_count(), (cudaStream_t)stream);
+  }
   if (use_v4(D, G, B)) {
     a.kmax = (int32_t)v4_kmax(max_ctx);
     const int64_t cb = v4_counter_bytes(B, p->kv_heads);
@@ -1316,6 +1353,12 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
   if (D == 64 && G == 1) return launch<64, 1>(a, B, st);
   set_error("tf_paged_decode_attn: unsupported head_dim %d / group %d", D, G);
   return TF_EINVAL;
+}
+
+int tf_paged_decode_attn_impl(int32_t impl) {
+  const int prev = attn_impl();
+  if (impl >= 1 && impl <= 5) g_impl = impl;
+  return prev;
 }
 
 }  // extern "C"

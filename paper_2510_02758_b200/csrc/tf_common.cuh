@@ -56,6 +56,8 @@ struct Pool {
   int64_t tile_elems;   // block_tokens * head_dim (one (block,layer,kv,head) tile)
   std::vector<int32_t> free_gpu, free_host;  // LIFO stacks (back = next)
   std::vector<uint8_t> used_gpu, used_host;  // per-block allocation state (double-free check)
+  alignas(64) unsigned char tmap[128];       // CUtensorMap of the HBM pool (v5 attention), built lazily
+  bool tmap_ok = false;
 
   // element offset of (block, layer, kv, head, slot, dim=0)
   __host__ __device__ int64_t off(int64_t b, int l, int kv, int h, int s) const {

@@ -87,95 +87,107 @@ def test_swap_rejects_bad_segments(cuda):
     p.close()
 
 
-def _attn_case(cuda, B, ctx_list, L, H, HQ, D, layer):
-    lib = _lib()
-    nblk_req = [(c + 15) // 16 for c in ctx_list]
-    nb = sum(nblk_req) + 3
-    p = _pool(cuda, nb, 1, L, H, D)
-    # bf16-valid random KV (randint bits could be NaN/Inf)
-    kv = (torch.randn(p.gpu.numel(), device=cuda) * 0.5).to(torch.bfloat16).view(torch.int16)
-    p.gpu.copy_(kv)
-    maxlb = max(nblk_req)
-    perm = np.random.default_rng(1).permutation(nb)
-    table = np.full((B, maxlb), -1, np.int32)
-    k = 0
-    for b in range(B):
-        table[b, : nblk_req[b]] = perm[k:k + nblk_req[b]]
-        k += nblk_req[b]
-    tab_d = torch.from_numpy(table).to(cuda)
-    rows = torch.arange(B, dtype=torch.int32, device=cuda)
-    ctx = torch.tensor(ctx_list, dtype=torch.int32, device=cuda)
-    q = (torch.randn(B, HQ, D, device=cuda)).to(torch.bfloat16)
-    out = torch.empty_like(q)
-    ws_n = max(1, int(lib.lib.tf_paged_decode_attn_workspace(p.handle, B, max(ctx_list), HQ)))
-    ws = torch.zeros(ws_n, dtype=torch.uint8, device=cuda)
-    lib.check(lib.lib.tf_paged_decode_attn(p.handle, C.c_void_p(q.data_ptr()), C.c_void_p(tab_d.data_ptr()), maxlb,
-                                           C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B, max(ctx_list),
-                                           layer, HQ, 1.0 / D ** 0.5, C.c_void_p(out.data_ptr()),
-                                           C.c_void_p(ws.data_ptr()), ws_n, None))
-    torch.cuda.synchronize()
-    pool = p.gpu_view().view(torch.bfloat16).float()
-    worst = 0.0
-    G = HQ // H
-    for b in range(B):
-        t = torch.arange(ctx_list[b], device=cuda)
-        blk = tab_d[b][(t // 16).long()].long()
-        kk = pool[blk, layer, 0, :, (t % 16).long()]  # [T][H][D]
-        vv = pool[blk, layer, 1, :, (t % 16).long()]
-        for h in range(HQ):
-            s = (kk[:, h // G, :] @ q[b, h].float()) / D ** 0.5
-            ref = torch.softmax(s.double(), 0).float() @ vv[:, h // G, :]
-            worst = max(worst, (out[b, h].float() - ref).abs().max().item())
-    p.close()
-    return worst
+_RNG = np.random.default_rng(5)
+# (contexts, layers, kv heads, q heads, head_dim, layer): C2 shapes (Llama3-8B
+# 32/8 hd128; Qwen2.5-32B TP=1 40/8) at batch 1 / 64 / 128 / 130 with ragged
+# 1-3000 contexts, block-edge contexts, the C1 tiny decoder (4/2 hd64)
+ATTN_CASES = {
+    "llama_b1": ([2049], 32, 8, 32, 128, 31),
+    "llama_edges": ([1, 15, 16, 17, 100, 700, 2049, 4000], 32, 8, 32, 128, 5),
+    "llama_b64_ragged": ([int(x) for x in _RNG.integers(1, 3000, 64)], 32, 8, 32, 128, 7),
+    "llama_b128_c2": ([int(x) for x in _RNG.integers(300, 900, 128)], 4, 8, 32, 128, 3),
+    "llama_b130_ragged": ([int(x) for x in _RNG.integers(1, 3000, 130)], 4, 8, 32, 128, 2),
+    "qwen_g5": ([17, 900, 4096, 1, 2500], 4, 8, 40, 128, 1),
+    "tiny_hd64": ([3, 64, 200, 513, 1000], 2, 2, 4, 64, 1),
+    "g8": ([33, 1000], 2, 4, 32, 128, 0),
+}
 
 
-@pytest.mark.parametrize("case", [
-    (8, [1, 15, 16, 17, 100, 700, 2049, 4000], 32, 8, 32, 128, 31),
-    (5, [3, 64, 200, 513, 1000], 2, 2, 4, 64, 1),
-    (3, [17, 900, 4096], 4, 8, 40, 128, 2),
-    (1, [1], 2, 2, 4, 64, 0),
-    # stream-K (v4): many warps per long segment, many segments per warp, ragged
-    (64, [int(x) for x in np.random.default_rng(5).integers(1, 3000, 64)], 32, 8, 32, 128, 7),
-    (130, [16 * (i % 9) + 1 + i for i in range(130)], 4, 8, 64, 128, 3),
-])
-def test_paged_attention_vs_fp32(cuda, case):
-    worst = _attn_case(cuda, *case)
-    assert worst <= 2e-2, worst  # bf16 output, fp32 accumulation (north-star tolerance)
+@pytest.mark.parametrize("impl", [5, 3])
+@pytest.mark.parametrize("name", list(ATTN_CASES))
+def test_paged_attention_vs_fp32(cuda, impl, name):
+    """Every row within 2e-2 of its own fp32 magnitude (attn_parity.py)."""
+    from attn_parity import run
+
+    ctx, L, H, HQ, D, layer = ATTN_CASES[name]
+    r = run(ctx, L, H, HQ, D, layer, impl=impl)
+    assert r <= 1.0, f"worst row error is {r:.2f}x the tolerance"
+
+
+@pytest.mark.parametrize("impl", [5, 3])
+def test_paged_attention_graph_plan_vs_fp32(cuda, impl):
+    """The CUDA-graph decode plan: launch captured ONCE for a 128-row bucket
+    with max_ctx = the pool maximum, padding rows on the scratch row; then the
+    real rows / contexts / q change on the device and the graph is replayed
+    (the workspace counters must self-reset between replays)."""
+    from attn_parity import REL_TOL, launch, make_case, worst_ratio
+    from paper_2510_02758_b200 import _lib as L_
+
+    prev = L_.lib.tf_paged_decode_attn_impl(impl)
+    try:
+        rng = np.random.default_rng(11)
+        ctx = [int(x) for x in rng.integers(1, 3000, 100)]
+        case = make_case(cuda, ctx, 3, 8, 32, 128, seed=3, pad_to=128, map_ctx=3000)
+        pool_max = 16 * 400  # the graphs plan for the pool's maximum context
+        st = torch.cuda.Stream()
+        out = torch.zeros_like(case["q"])
+        ws_n = max(1, int(L_.lib.tf_paged_decode_attn_workspace(case["pool"].handle, 128, pool_max, 32)))
+        ws = torch.zeros(ws_n, dtype=torch.uint8, device=cuda)
+        with torch.cuda.stream(st):
+            launch(case, 1, max_ctx=pool_max, out=out, ws=ws, stream=st)  # warm-up (attributes, tensor map)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            launch(case, 1, max_ctx=pool_max, out=out, ws=ws, stream=torch.cuda.current_stream())
+        for rep in range(3):
+            # new contexts (a different ragged batch) and new q, same buffers
+            new = [int(x) for x in rng.integers(1, 3000, 100)]
+            case["ctx"][:100].copy_(torch.tensor(new, dtype=torch.int32))
+            case["q"].copy_((torch.randn_like(case["q"].float()) * 4).to(torch.bfloat16))
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            r = worst_ratio(case, 1, out)
+            assert r <= 1.0, f"replay {rep}: worst row error {r:.2f}x the {REL_TOL} tolerance"
+        case["pool"].close()
+    finally:
+        L_.lib.tf_paged_decode_attn_impl(prev)
+
+
+@pytest.mark.parametrize("impl", [5, 3])
+def test_paged_attention_parity_catches_a_dropped_split(cuda, impl):
+    """The parity check can fail: with TF_ATTN_MUTATE=1 every (request, kv
+    head) of >= 8 blocks ignores its last eighth (a lost split); the same
+    check run in a subprocess must report a violation at C2 contexts."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, 'tests'); from attn_parity import run; "
+            f"print(run([2049, 4000, 700, 1500], 4, 8, 32, 128, 2, impl={impl}))")
+    env = dict(os.environ, TF_ATTN_MUTATE="1")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                         cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    assert res.returncode == 0, res.stderr[-2000:]
+    ratio = float(res.stdout.strip().splitlines()[-1])
+    assert ratio > 1.0, f"mutated kernel passed the parity check (ratio {ratio:.2f})"
 
 
 def test_paged_attention_workspace_reuse_is_deterministic(cuda):
     """The stream-K merge counters reset themselves: relaunching with the same
     workspace gives bit-identical outputs (merge order is fixed by slot)."""
-    lib = _lib()
-    B, L, H, HQ, D = 48, 2, 8, 32, 128
-    ctx_list = [int(x) for x in np.random.default_rng(9).integers(1, 2500, B)]
-    nblk_req = [(c + 15) // 16 for c in ctx_list]
-    p = _pool(cuda, sum(nblk_req) + 1, 1, L, H, D)
-    p.gpu.copy_((torch.randn(p.gpu.numel(), device=cuda) * 0.5).to(torch.bfloat16).view(torch.int16))
-    maxlb = max(nblk_req)
-    table = np.full((B, maxlb), -1, np.int32)
-    k = 0
-    for b in range(B):
-        table[b, : nblk_req[b]] = np.arange(k, k + nblk_req[b])
-        k += nblk_req[b]
-    tab_d = torch.from_numpy(table).to(cuda)
-    rows = torch.arange(B, dtype=torch.int32, device=cuda)
-    ctx = torch.tensor(ctx_list, dtype=torch.int32, device=cuda)
-    q = torch.randn(B, HQ, D, device=cuda).to(torch.bfloat16)
-    ws_n = max(1, int(lib.lib.tf_paged_decode_attn_workspace(p.handle, B, 4096, HQ)))
-    ws = torch.zeros(ws_n, dtype=torch.uint8, device=cuda)
-    outs = []
-    for _ in range(3):
-        out = torch.empty_like(q)
-        lib.check(lib.lib.tf_paged_decode_attn(p.handle, C.c_void_p(q.data_ptr()), C.c_void_p(tab_d.data_ptr()),
-                                               maxlb, C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B,
-                                               4096, 1, HQ, 1.0 / D ** 0.5, C.c_void_p(out.data_ptr()),
-                                               C.c_void_p(ws.data_ptr()), ws_n, None))
-        outs.append(out)
+    from attn_parity import launch, make_case
+
+    ctx_list = [int(x) for x in np.random.default_rng(9).integers(1, 2500, 48)]
+    case = make_case(cuda, ctx_list, 2, 8, 32, 128, seed=4)
+    out0, ws = launch(case, 1, max_ctx=4096)
+    outs = [out0.clone()]
+    for _ in range(2):
+        o, _ = launch(case, 1, max_ctx=4096, ws=ws)
+        outs.append(o.clone())
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
-    p.close()
+    case["pool"].close()
 
 
 def test_kv_append_writes_slots(cuda):

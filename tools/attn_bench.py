@@ -81,6 +81,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--batches", default="32,64,96,128")
     ap.add_argument("--plans", default="exact,pool")
+    ap.add_argument("--impls", default="5", help="comma list of implementations (tf_paged_decode_attn_impl)")
     args = ap.parse_args()
     dev = torch.device("cuda")
     pool = KvPool(22000, 1, 32, 8, 128, device=dev)
@@ -91,17 +92,20 @@ def main():
     for B in [int(x) for x in args.batches.split(",")]:
         for name, ctxs in (("uniform2600", [2600] * B),
                            ("ragged500-3000", list(rng.integers(500, 3000, B))),
-                           ("short736", list(rng.integers(600, 870, B)))):
+                           ("short736", list(rng.integers(600, 870, B))),
+                           ("c2live560", list(rng.integers(200, 920, B)))):
             for plan in args.plans.split(","):
                 if args.only and args.only != f"{B}:{name}:{plan}":
                     continue
                 plan_ctx = max(ctxs) if plan == "exact" else 4096
-                ms, ab = run_case(pool, B, [int(c) for c in ctxs], plan_ctx, reps=args.reps)
-                gbs = ab / (ms / 1e3) / 1e9
-                row = {"B": B, "ctx": name, "plan": plan, "us": round(ms * 1e3, 2), "MB": round(ab / 1e6, 1),
-                       "gbs": round(gbs, 1), "frac": round(gbs / pk, 4)}
-                cases.append(row)
-                print(json.dumps(row), flush=True)
+                for impl in [int(x) for x in args.impls.split(",")]:
+                    _lib.lib.tf_paged_decode_attn_impl(impl)
+                    ms, ab = run_case(pool, B, [int(c) for c in ctxs], plan_ctx, reps=args.reps)
+                    gbs = ab / (ms / 1e3) / 1e9
+                    row = {"impl": impl, "B": B, "ctx": name, "plan": plan, "us": round(ms * 1e3, 2),
+                           "MB": round(ab / 1e6, 1), "gbs": round(gbs, 1), "frac": round(gbs / pk, 4)}
+                    cases.append(row)
+                    print(json.dumps(row), flush=True)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps({"peak_gbs": pk, "cases": cases}, indent=1))
 
