@@ -159,14 +159,16 @@ int tf_q_fill_synthetic(void* q, const int32_t* dev_rids, const int32_t* dev_pos
  * paged KV of layer `layer` of request row rows[b]; GQA head h reads kv head
  * h / (n_q_heads/kv_heads).  q/out: [B][n_q_heads][head_dim] bf16, fp32
  * accumulation on tensor cores (mma.sync bf16 for the QK^T / PV contractions).
- * Default implementation (v5, tf_attn_tma.cu; head_dim 128 with group 1/2/4/
- * 5/8 or head_dim 64 with group 1/2/4, B <= 1024): a persistent grid of
- * stream-K warps - the layer's (request, kv head, block) work is split evenly
- * over the warps; each warp's elected lane streams its 16-token K/V tiles
- * with TMA tensor loads (128-B swizzle) into a per-warp mbarrier ring, running
- * ahead across (request, head) boundaries; a (request, head) shared by
- * several warps is merged in-kernel by the last warp to finish.  Other shapes
- * use the split-KV kernel (v3, head_dim 128) or the CUDA-core kernels.
+ * Implementations (tf_paged_decode_attn_impl): v5 (tf_attn_tma.cu; head_dim
+ * 128 with group 1/2/4/5/8 or head_dim 64 with group 1/2/4, B <= 1024) is a
+ * persistent grid of stream-K warps - the layer's (request, kv head, block)
+ * work is split evenly over the warps; each warp's elected lane streams its
+ * 16-token K/V tiles with TMA tensor loads (128-B swizzle) into a per-warp
+ * mbarrier ring, running ahead across (request, head) boundaries; a (request,
+ * head) shared by several warps is merged in-kernel.  v3 (head_dim 128) is a
+ * split-KV grid of (request, kv head, split) CTAs with cp.async rings.  The
+ * default picks v5 for B <= 64 and v3 above (faster there on B200); other
+ * shapes use the CUDA-core kernels.
  * max_ctx must bound every ctx[b].  The workspace (size from
  * tf_paged_decode_attn_workspace for the same B / max_ctx / n_q_heads, under
  * the same implementation) must be ZERO-filled before its first use; every
@@ -178,9 +180,10 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
                          int32_t layer, int32_t n_q_heads, float scale, void* out, void* workspace,
                          int64_t workspace_bytes, void* stream);
 int64_t tf_paged_decode_attn_workspace(int64_t pool, int32_t B, int32_t max_ctx, int32_t n_q_heads);
-/* Select the implementation for subsequent launches (1..5; see above; any
- * other value only queries).  Returns the previous selection.  For A/B
- * benchmarks and for tests that check every implementation in one process. */
+/* Select the implementation for subsequent launches (0 = the default by
+ * batch, 1..5 = that version; any other value only queries).  Returns the
+ * previous selection.  For A/B benchmarks and for tests that check every
+ * implementation in one process. */
 int tf_paged_decode_attn_impl(int32_t impl);
 
 /* ----------------------------------------------------------------- selector --

@@ -1127,18 +1127,25 @@ __global__ void __launch_bounds__(kV4Warps * 32, kV4CtasPerSm) paged_attn_stream
   end_segment(seg);
 }
 
-// implementation selector: 5 (default) = TMA stream-K (tf_attn_tma.cu), 3 =
-// split-KV cp.async tensor-core kernel, 4 = cp.async stream-K, 2 = bulk-copy
-// CUDA-core, 1 = register-staged CUDA-core.  TF_ATTN_IMPL overrides the default
-// at start-up; tf_paged_decode_attn_impl() switches it at run time (A/B
-// benchmarks and the parity tests run every implementation in one process).
+// implementation selector: 0 (default) = by batch - v5 (TMA stream-K,
+// tf_attn_tma.cu) for B <= 64, v3 above (measured: profiles/r2_attn_*.json);
+// 5 = v5, 3 = split-KV cp.async tensor-core kernel, 4 = cp.async stream-K,
+// 2 = bulk-copy CUDA-core, 1 = register-staged CUDA-core.  TF_ATTN_IMPL
+// overrides the default at start-up; tf_paged_decode_attn_impl() switches it
+// at run time (A/B benchmarks and the parity tests run every implementation
+// in one process).
 static int g_impl = -1;
-static int attn_impl() {
+static int attn_impl_sel() {
   if (g_impl < 0) {
     const char* e = getenv("TF_ATTN_IMPL");
-    g_impl = (e && e[0] >= '1' && e[0] <= '5') ? e[0] - '0' : 5;
+    g_impl = (e && e[0] >= '1' && e[0] <= '5') ? e[0] - '0' : 0;
   }
   return g_impl;
+}
+static thread_local int g_cur_b = 0;  // batch of the launch being planned (for the "by batch" default)
+static int attn_impl() {
+  const int i = attn_impl_sel();
+  return i ? i : (g_cur_b <= 64 ? 5 : 3);
 }
 
 // test-only fault injection (TF_ATTN_MUTATE=1: every (request, kv head) with
@@ -1265,6 +1272,7 @@ int64_t tf_paged_decode_attn_workspace(int64_t pool, int32_t B, int32_t max_ctx,
   if (!p) return -1;
   if (n_q_heads % p->kv_heads) return -1;
   const int G = n_q_heads / p->kv_heads;
+  g_cur_b = B;
   if (attn_impl() == 5 && attn5_supported(p, G, B)) return attn5_workspace(p, B, max_ctx, G);
   if (use_v4(p->head_dim, G, B))
     return v4_counter_bytes(B, p->kv_heads) +
@@ -1303,6 +1311,7 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
   a.scale_log2 = scale * 1.4426950408889634f;
   const int G = n_q_heads / p->kv_heads;
   const int D = p->head_dim;
+  g_cur_b = B;
   a.B = B;
   a.mutate = attn_mutate();
   if (attn_impl() == 5 && attn5_supported(p, G, B)) {
@@ -1356,8 +1365,8 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
 }
 
 int tf_paged_decode_attn_impl(int32_t impl) {
-  const int prev = attn_impl();
-  if (impl >= 1 && impl <= 5) g_impl = impl;
+  const int prev = attn_impl_sel();
+  if (impl >= 0 && impl <= 5) g_impl = impl;
   return prev;
 }
 

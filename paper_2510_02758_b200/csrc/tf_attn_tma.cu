@@ -125,33 +125,20 @@ __device__ __forceinline__ void cur_advance(const int* pre, int B, int kv, Curso
   } while (c.nb == 0);
 }
 
-// G = q heads per kv head (<= 8), NH = head_dim / 64, S = ring stages per warp
-template <int G, int NH, int S, int W, int CPS>
-__global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __grid_constant__ CUtensorMap map,
-                                                                        const Attn5Args a) {
-  constexpr int D = 64 * NH;
-  constexpr uint32_t kHalf = kBlk5 * 64 * 2;          // one [16][64] bf16 box = 2 KiB
-  constexpr uint32_t kStage = 2 * NH * kHalf;         // K and V of one block
-  static_assert(G >= 1 && G <= 8, "the group fills the N=8 side of the tile");
-  extern __shared__ __align__(1024) unsigned char smem5[];
-  __shared__ int pre[kAttn5MaxB + 1];
-  __shared__ __align__(8) uint64_t bars[W][S];
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  // 1024-B aligned ring (the 128-B swizzle pattern repeats every 1024 B)
-  const uint32_t ring_base = (s_u32(smem5) + 1023u) & ~1023u;
-  const uint32_t ring = ring_base + (uint32_t)warp * S * kStage;
-  const int B = a.B, kv = a.kv_heads;
-
-  if (threadIdx.x < W * S) mbar_init5(&bars[threadIdx.x / S][threadIdx.x % S], 1);
-  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  // blocks per request -> prefix sums (every CTA; B <= 1024)
-  if (warp == 0) {
+// blocks per request -> prefix sums in shared memory (B <= 1024).  Every
+// thread of the CTA loads its share of the contexts first (ONE memory round
+// trip, not B/32 dependent ones), then warp 0 scans them; ends with a CTA barrier.
+template <int NT>
+__device__ __forceinline__ void block_prefix(const int32_t* __restrict__ ctx, int B, int* pre) {
+  for (int b = threadIdx.x; b < B; b += NT) pre[b + 1] = (__ldg(ctx + b) + kBlk5 - 1) / kBlk5;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     int carry = 0;
     if (lane == 0) pre[0] = 0;
     for (int base = 0; base < B; base += 32) {
       const int b = base + lane;
-      int v = b < B ? (__ldg(a.ctx + b) + kBlk5 - 1) / kBlk5 : 0;
+      int v = b < B ? pre[b + 1] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(0xffffffffu, v, o);
@@ -162,31 +149,100 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
     }
   }
   __syncthreads();
+}
+
+// Programmatic dependent launch (PDL): the prologue of a launch overlaps the
+// tail of the kernel before it on the stream; griddep_wait() blocks until
+// that kernel has completed and its writes are visible.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// G = q heads per kv head (<= 8), NH = head_dim / 64, S = ring stages per
+// warp, W = warps per CTA, CPS = CTAs per SM
+template <int G, int NH, int S, int W, int CPS>
+__global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __grid_constant__ CUtensorMap map,
+                                                                        const Attn5Args a) {
+  constexpr int D = 64 * NH;
+  constexpr uint32_t kHalf = kBlk5 * 64 * 2;          // one [16][64] bf16 box = 2 KiB
+  constexpr uint32_t kStage = 2 * NH * kHalf;         // K and V of one block
+  static_assert(G >= 1 && G <= 8, "the group fills the N=8 side of the tile");
+  extern __shared__ __align__(1024) unsigned char smem5[];
+  __shared__ int pre[kAttn5MaxB + 1];
+  __shared__ int rows_sh[kAttn5MaxB];
+  __shared__ __align__(8) uint64_t bars[W][S];
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  // 1024-B aligned ring (the 128-B swizzle pattern repeats every 1024 B)
+  const uint32_t ring_base = (s_u32(smem5) + 1023u) & ~1023u;
+  const uint32_t ring = ring_base + (uint32_t)warp * S * kStage;
+  const int B = a.B, kv = a.kv_heads;
+
+  // ---- prologue: reads only what the kernels BEFORE the previous one wrote
+  // (contexts, rows, block tables), so under PDL it overlaps that kernel
+  __shared__ int lid_sh;
+  if (threadIdx.x < W * S) mbar_init5(&bars[threadIdx.x / S][threadIdx.x % S], 1);
+  if (threadIdx.x == 0) {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
+    // logical CTA index in DISPATCH order (ticket): a warp only ever waits on
+    // warps of lower logical index, which are resident or finished - no
+    // deadlock even when other kernels share the SMs
+    lid_sh = (int)(atomicAdd(a.ticket, 1ull) % gridDim.x);
+  }
+  for (int b = threadIdx.x; b < B; b += W * 32) rows_sh[b] = __ldg(a.rows + b);
+  block_prefix<W * 32>(a.ctx, B, pre);
   const int T = pre[B] * kv;
   const int NWt = gridDim.x * W;
   const int per = max(a.min_per, (T + NWt - 1) / NWt);
-  const int gw = blockIdx.x * W + warp;
+  const int gw = lid_sh * W + warp;
   const int lo = gw * per;
-  if (lo >= T) return;
   const int hi = min(T, lo + per);
   const int n = hi - lo;
   uint64_t* bar = bars[warp];
 
-  // ---------------------------------------------------------------- producer
-  // (lane 0 only: its own issue cursor, S-1 blocks ahead of the math)
-  Cursor ic;
-  int ic_rowb = -1;
-  const int32_t* itrow = nullptr;
-  if (lane == 0) cur_locate(pre, B, kv, lo, ic);
+  // Processing order: the range is ROTATED to start at its tail piece (the
+  // first part of a segment continued by higher warps) and wrap to `lo`, so
+  // both split pieces of every warp are done first and their partials are
+  // published long before anyone merges them.  rot = offset of that piece.
+  int rot = 0;
+  if (n > 0) {
+    Cursor t;
+    cur_locate(pre, B, kv, hi - 1, t);
+    const int seg_lo = hi - 1 - t.j;  // first position of the last segment touched
+    if (t.j != t.nb - 1 && seg_lo > lo) rot = seg_lo - lo;  // partial tail piece, not the whole range
+  }
+  auto pos_of = [&](int r) { return lo + (r + rot < n ? r + rot : r + rot - n); };
+
+  // Block ids of this warp's range, 32 at a time: lane L of chunk c holds the
+  // packed (block << 8 | kv head) of sequence index 32c + L.  Two chunks live
+  // in registers; the next is loaded 32 issues before it is needed, so the
+  // dependent table load is never on the critical path.
+  auto load_chunk = [&](int c) -> int {
+    const int r = 32 * c + lane;
+    if (r >= n) return 0;
+    Cursor t;
+    cur_locate(pre, B, kv, pos_of(r), t);
+    return (__ldg(a.table + (int64_t)rows_sh[t.b] * a.stride + t.j) << 8) | t.kvh;
+  };
+  int e_cur = 0, e_nxt = 0, cur_chunk = 0;
+  if (n > 0) {
+    e_cur = load_chunk(0);
+    e_nxt = load_chunk(1);
+  }
+  // everything below reads q / the KV the previous kernel (rope + append) wrote
+  griddep_wait();
+  if (n <= 0) return;
+
   const int64_t tile_rows = (int64_t)kv * kBlk5;  // rows between K and V of one layer
-  auto issue = [&](int i) {
-    if (lane == 0 && i < n) {
-      if (ic.b != ic_rowb) {
-        ic_rowb = ic.b;
-        itrow = a.table + (int64_t)__ldg(a.rows + ic.b) * a.stride;
-      }
-      const int64_t blk = __ldg(itrow + ic.j);
-      const int64_t krow = (((blk * a.n_layers + a.layer) * 2) * kv + ic.kvh) * kBlk5;
+  auto issue = [&](int i) {  // all lanes (uniform); lane 0 issues the TMA
+    if (i >= n) return;
+    if (i == 32 * (cur_chunk + 1)) {  // all of cur_chunk issued: rotate, fetch chunk + 2
+      e_cur = e_nxt;
+      ++cur_chunk;
+      e_nxt = load_chunk(cur_chunk + 1);
+    }
+    const int e = __shfl_sync(0xffffffffu, e_cur, i & 31);
+    if (lane == 0) {
+      const int64_t krow = ((((int64_t)(e >> 8) * a.n_layers + a.layer) * 2) * kv + (e & 255)) * kBlk5;
       const int s = i % S;
       const uint32_t dst = ring + s * kStage;
       mbar_expect_tx5(&bar[s], kStage);
@@ -203,7 +259,6 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
             "l"(reinterpret_cast<uint64_t>(&map)), "r"(0), "r"(h), "r"((int)(krow + tile_rows)), "r"(s_u32(&bar[s]))
             : "memory");
       }
-      cur_advance(pre, B, kv, ic);
     }
   };
 #pragma unroll
@@ -213,31 +268,64 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
   const int g4 = lane >> 2, q4 = lane & 3;  // fragment row group / quad index
   const int h0 = 2 * q4;                    // this thread's two heads: h0, h0 + 1
   Cursor cc, seg;
-  cur_locate(pre, B, kv, lo, cc);
+  cur_locate(pre, B, kv, pos_of(0), cc);
   uint32_t qb[4 * NH][2];  // B operand Q^T: head g4, dims 16kk + 2q4 (+1), (+8)
   float o[4 * NH][4];      // O^T accumulators: dims 16mt + g4 (+8), heads h0, h0+1
   float m_0 = -FLT_MAX, m_1 = -FLT_MAX, l_0 = 0.f, l_1 = 0.f;
   int ctx = 0, ctx_eff = 0;
 
+  uint32_t qn[4 * NH][2];  // the NEXT segment's q fragments, loaded one segment ahead
+  auto load_q = [&](int b, int kvh) {
+    const uint16_t* qrow = a.q + ((int64_t)b * a.hq + kvh * G + (g4 < G ? g4 : 0)) * D + 2 * q4;
+#pragma unroll
+    for (int kk = 0; kk < 4 * NH; ++kk) {
+      qn[kk][0] = g4 < G ? *reinterpret_cast<const unsigned int*>(qrow + kk * 16) : 0u;
+      qn[kk][1] = g4 < G ? *reinterpret_cast<const unsigned int*>(qrow + kk * 16 + 8) : 0u;
+    }
+  };
+  load_q(cc.b, cc.kvh);
   auto begin_segment = [&]() {
     seg = cc;
     ctx = __ldg(a.ctx + cc.b);
     ctx_eff = ctx;
     if (a.mutate == 1 && cc.nb >= 8) ctx_eff = min(ctx, (cc.nb - cc.nb / 8) * kBlk5);  // test-only: drop 1/8
-    const uint16_t* qrow = a.q + ((int64_t)cc.b * a.hq + cc.kvh * G + (g4 < G ? g4 : 0)) * D + 2 * q4;
 #pragma unroll
     for (int kk = 0; kk < 4 * NH; ++kk) {
-      qb[kk][0] = g4 < G ? __ldg(reinterpret_cast<const unsigned int*>(qrow + kk * 16)) : 0u;
-      qb[kk][1] = g4 < G ? __ldg(reinterpret_cast<const unsigned int*>(qrow + kk * 16 + 8)) : 0u;
+      qb[kk][0] = qn[kk][0];
+      qb[kk][1] = qn[kk][1];
     }
+    // prefetch the next segment's q (first used >= 1 block later)
+    Cursor nx = cc;
+    nx.j = nx.nb - 1;
+    cur_advance(pre, B, kv, nx);
+    if (nx.b < B) load_q(nx.b, nx.kvh);
 #pragma unroll
     for (int mt = 0; mt < 4 * NH; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
     m_0 = m_1 = -FLT_MAX;
     l_0 = l_1 = 0.f;
   };
 
-  auto end_segment = [&](const Cursor& sc) {
-    // row sums over the 8 token groups
+  // A segment wholly inside this warp is normalised and stored.  A segment
+  // split over warps first..last: every piece leaves its fp32 partial
+  // (accumulator, max, sum) in slot gw - first; the pieces below `last`
+  // publish theirs (fence + counter increment) two blocks LATER, when their
+  // stores have completed (cheap fence, no stall on the stream); warp `last`
+  // merges at its end, after waiting on the counter (only lower warps, see
+  // the ticket).  With the rotated order every published piece is one of a
+  // warp's first two, so the merger practically never waits.
+  int pub_sid = -1, pub_at = 0;     // partial written, published at iteration pub_at
+  int mrg_sid = -1, mrg_cnt = 0, mrg_b = 0, mrg_kvh = 0;  // segment this warp merges at its end
+  auto publish = [&]() {
+    if (pub_sid < 0) return;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(a.counters + pub_sid, 1);
+    }
+    pub_sid = -1;
+  };
+  auto end_segment = [&](const Cursor& sc, int i_now) {
+    publish();
     float l0 = l_0, l1 = l_1;
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
@@ -247,7 +335,7 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
     const int Sg = pre[sc.b] * kv + sc.kvh * sc.nb;
     const int first = Sg / per, last = (Sg + sc.nb - 1) / per;
     const int64_t row0 = (int64_t)sc.b * a.hq + sc.kvh * G;
-    if (first == last) {  // the whole segment is this warp's: normalise and store
+    if (first == last) {
       const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
 #pragma unroll
       for (int mt = 0; mt < 4 * NH; ++mt) {
@@ -264,8 +352,7 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
       return;
     }
     const int sid = sc.b * kv + sc.kvh;
-    const int64_t slot0 = (int64_t)sid * a.kmax;
-    const int64_t slot = slot0 + (gw - first);
+    const int64_t slot = (int64_t)sid * a.kmax + (gw - first);
 #pragma unroll
     for (int mt = 0; mt < 4 * NH; ++mt) {
       const int d = 16 * mt + g4;
@@ -279,25 +366,32 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
       }
     }
     if (g4 == 0) {
-      if (h0 < G) {
-        a.ws_ml[(slot * G + h0) * 2 + 0] = m_0;
-        a.ws_ml[(slot * G + h0) * 2 + 1] = l0;
-      }
-      if (h0 + 1 < G) {
-        a.ws_ml[(slot * G + h0 + 1) * 2 + 0] = m_1;
-        a.ws_ml[(slot * G + h0 + 1) * 2 + 1] = l1;
-      }
+      if (h0 < G) *reinterpret_cast<float2*>(a.ws_ml + (slot * G + h0) * 2) = make_float2(m_0, l0);
+      if (h0 + 1 < G) *reinterpret_cast<float2*>(a.ws_ml + (slot * G + h0 + 1) * 2) = make_float2(m_1, l1);
     }
-    __threadfence();
+    if (gw == last) {
+      mrg_sid = sid;
+      mrg_cnt = last - first + 1;
+      mrg_b = sc.b;
+      mrg_kvh = sc.kvh;
+    } else {
+      pub_sid = sid;
+      pub_at = i_now + 2;
+    }
+  };
+
+  auto merge = [&]() {
+    // wait until the cnt - 1 lower pieces are published (acquire), then merge
+    if (lane == 0) {
+      unsigned int v = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.counters + mrg_sid) : "memory");
+      } while ((int)v != mrg_cnt - 1);
+    }
     __syncwarp();
-    int old = 0;
-    if (lane == 0) old = atomicAdd(a.counters + sid, 1);
-    old = __shfl_sync(0xffffffffu, old, 0);
-    const int cnt = last - first + 1;
-    if (old != cnt - 1) return;
-    // last of the segment's warps: merge the cnt partials; lane owns G*D/32
-    // consecutive elements of the [G][D] tile, in float4s (never straddling a row)
-    __threadfence();
+    const int64_t slot0 = (int64_t)mrg_sid * a.kmax;
+    const int64_t row0 = (int64_t)mrg_b * a.hq + mrg_kvh * G;
+    // lane owns G*D/32 consecutive elements of the [G][D] tile, in float4s
     constexpr int E = G * D / 32;
     constexpr int NC = (E + 3) / 4;
     float mrow[NC], lsum[NC];
@@ -308,23 +402,22 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
       lsum[c] = 0.f;
       acc4[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    for (int k = 0; k < cnt; ++k) {
+    for (int k = 0; k < mrg_cnt; ++k) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const int e = lane * E + 4 * c;
         if (4 * c < E) mrow[c] = fmaxf(mrow[c], __ldcg(a.ws_ml + ((slot0 + k) * G + e / D) * 2));
       }
     }
-    for (int k = 0; k < cnt; ++k) {
+    for (int k = 0; k < mrg_cnt; ++k) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         if (4 * c >= E) continue;
         const int e = lane * E + 4 * c, g = e / D, d = e % D;
-        const float mk = __ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2);
-        const float lk = __ldcg(a.ws_ml + ((slot0 + k) * G + g) * 2 + 1);
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.ws_ml + ((slot0 + k) * G + g) * 2));
         const float4 v = __ldcg(reinterpret_cast<const float4*>(a.ws_acc + ((slot0 + k) * G + g) * D + d));
-        const float w = mk == -FLT_MAX ? 0.f : exp2f(mk - mrow[c]);
-        lsum[c] += lk * w;
+        const float w = ml.x == -FLT_MAX ? 0.f : exp2f(ml.x - mrow[c]);
+        lsum[c] += ml.y * w;
         acc4[c].x += v.x * w;
         acc4[c].y += v.y * w;
         acc4[c].z += v.z * w;
@@ -341,7 +434,7 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
       pk.y = pk_bf16(acc4[c].z * inv, acc4[c].w * inv);
       *reinterpret_cast<uint2*>(a.out + (row0 + g) * D + d) = pk;
     }
-    if (lane == 0) a.counters[sid] = 0;  // ready for the next launch (and graph replay)
+    if (lane == 0) a.counters[mrg_sid] = 0;  // every piece has arrived: ready for the next launch
   };
 
   // ldmatrix lane addressing inside a [16 rows][64] swizzled box
@@ -353,10 +446,15 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
 
   begin_segment();
   for (int i = 0; i < n; ++i) {
-    if (i > 0 && cc.j == 0) {  // crossed into the next (request, kv head)
-      end_segment(seg);
+    if (i > 0 && (cc.j == 0 || i == n - rot)) {  // next (request, kv head), or the wrap to `lo`
+      end_segment(seg, i);
+      if (i == n - rot) {  // wrap: the head piece at `lo` (its q was not the prefetched successor)
+        cur_locate(pre, B, kv, lo, cc);
+        load_q(cc.b, cc.kvh);
+      }
       begin_segment();
     }
+    if (i == pub_at) publish();
     issue(i + S - 1);
     const int s = i % S;
     mbar_wait5(&bar[s], (uint32_t)((i / S) & 1));
@@ -430,7 +528,29 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
     if (valid < kBlk5 && lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     cur_advance(pre, B, kv, cc);
   }
-  end_segment(seg);
+  end_segment(seg, n);
+  publish();
+  if (mrg_sid >= 0) merge();
+}
+
+// launched with the PDL attribute: the prologue may run while the previous
+// kernel on the stream drains (griddepcontrol.wait before touching its
+// outputs); captured into CUDA graphs as a programmatic edge
+template <typename K, typename... Args>
+int launch_pdl(K kernel, dim3 grid, dim3 block, int smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TF_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+  TF_LAUNCH_CHECK();
+  return TF_OK;
 }
 
 template <int G, int NH, int S, int W, int CPS>
@@ -443,9 +563,7 @@ int launch5(const CUtensorMap& map, const Attn5Args& a, int sms, cudaStream_t st
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  paged_attn_tma5_kernel<G, NH, S, W, CPS><<<sms * CPS, W * 32, smem, st>>>(map, a);
-  TF_LAUNCH_CHECK();
-  return TF_OK;
+  return launch_pdl(paged_attn_tma5_kernel<G, NH, S, W, CPS>, dim3(sms * CPS), dim3(W * 32), smem, st, map, a);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -506,7 +624,8 @@ int64_t attn5_kmax(int max_ctx) {
   return (std::max(1, (max_ctx + kBlk5 - 1) / kBlk5) + kAttn5MinPer - 1) / kAttn5MinPer + 1;
 }
 
-int64_t attn5_counter_bytes(int B, int kv) { return ((int64_t)B * kv * 4 + 255) / 256 * 256; }
+// workspace: [ticket u64 | pad to 256][merge counters B*kv int32, to 256][(max, sum) partials][acc partials]
+int64_t attn5_counter_bytes(int B, int kv) { return 256 + ((int64_t)B * kv * 4 + 255) / 256 * 256; }
 
 int64_t attn5_workspace(const Pool* p, int B, int max_ctx, int G) {
   return attn5_counter_bytes(B, p->kv_heads) +
@@ -524,27 +643,36 @@ int attn5_launch(Pool* p, Attn5Args a, int G, int max_ctx, void* workspace, int6
   const int64_t need = attn5_workspace(p, a.B, max_ctx, G);
   TF_CHECK_ARG(workspace && workspace_bytes >= need, "tf_paged_decode_attn: workspace too small (%lld < %lld)",
                (long long)workspace_bytes, (long long)need);
-  a.counters = (int32_t*)workspace;
+  a.ticket = (unsigned long long*)workspace;
+  a.counters = (int32_t*)((char*)workspace + 256);
   a.ws_ml = (float*)((char*)workspace + cb);
   a.ws_acc = a.ws_ml + (int64_t)a.B * p->kv_heads * a.kmax * G * 2;
   a.n_layers = p->n_layers;
   a.kv_heads = p->kv_heads;
-  // S = 3 stages per warp (2 blocks in flight), 4 warps per CTA, 2 CTAs per SM
+  a.pool = p->gpu;
+  // ring configuration (TF_ATTN5_CFG): 1 (default) = 2 stages per warp x 4
+  // warps x 3 CTAs per SM (12 warps, 24 blocks = 192 KiB in flight per SM);
+  // 0 = 3 stages x 4 warps x 2 CTAs (8 warps, 16 blocks in flight): cfg 1 is
+  // 3-5% faster at B = 64-128 (profiles/r2_attn_cfg.json)
+  static const int cfg = getenv("TF_ATTN5_CFG") ? atoi(getenv("TF_ATTN5_CFG")) : 1;
+#define TF_A5(G_, NH_) \
+  return cfg == 1 ? launch5<G_, NH_, 2, 4, 3>(*map, a, sms, st) : launch5<G_, NH_, 3, 4, 2>(*map, a, sms, st)
   if (p->head_dim == 128) {
     switch (G) {
-      case 1: return launch5<1, 2, 3, 4, 2>(*map, a, sms, st);
-      case 2: return launch5<2, 2, 3, 4, 2>(*map, a, sms, st);
-      case 4: return launch5<4, 2, 3, 4, 2>(*map, a, sms, st);
-      case 5: return launch5<5, 2, 3, 4, 2>(*map, a, sms, st);
-      case 8: return launch5<8, 2, 3, 4, 2>(*map, a, sms, st);
+      case 1: TF_A5(1, 2);
+      case 2: TF_A5(2, 2);
+      case 4: TF_A5(4, 2);
+      case 5: TF_A5(5, 2);
+      case 8: TF_A5(8, 2);
     }
   } else {
     switch (G) {
-      case 1: return launch5<1, 1, 3, 4, 2>(*map, a, sms, st);
-      case 2: return launch5<2, 1, 3, 4, 2>(*map, a, sms, st);
-      case 4: return launch5<4, 1, 3, 4, 2>(*map, a, sms, st);
+      case 1: TF_A5(1, 1);
+      case 2: TF_A5(2, 1);
+      case 4: TF_A5(4, 1);
     }
   }
+#undef TF_A5
   set_error("tf_paged_decode_attn: v5 has no instance for head_dim %d / group %d", p->head_dim, G);
   return TF_EINVAL;
 }

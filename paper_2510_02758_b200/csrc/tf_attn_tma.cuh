@@ -8,6 +8,7 @@ constexpr int kAttn5MaxB = 1024;  // requests per launch (prefix sums in shared 
 constexpr int kAttn5MinPer = 4;   // minimum blocks per warp (bounds the partials per segment)
 
 struct Attn5Args {
+  const uint16_t* pool;  // HBM pool base (L2 prefetch addresses)
   const uint16_t* q;
   const int32_t* table;
   const int32_t* rows;
@@ -16,6 +17,7 @@ struct Attn5Args {
   float* ws_acc;      // [B*kv][kmax][G][D] partial accumulators
   float* ws_ml;       // [B*kv][kmax][G][2] partial (max, sum)
   int32_t* counters;  // [B*kv] self-resetting merge counters
+  unsigned long long* ticket;  // dispatch-order CTA ticket (monotonic; grid size is fixed per process)
   int32_t stride, n_layers, kv_heads, layer, hq, B, kmax, min_per;
   float scale_log2;
   int32_t mutate;     // test-only fault injection (TF_ATTN_MUTATE), 0 in production

@@ -115,7 +115,7 @@ def worst_ratio(case, layer, out, rows=None):
 def run(ctx_list, L, H, HQ, D, layer, impl=None, pad_to=None, max_ctx=None, seed=0):
     """-> worst ratio for one launch (used by the mutation subprocess)."""
     lib = _lib()
-    prev = lib.lib.tf_paged_decode_attn_impl(impl or 0)
+    prev = lib.lib.tf_paged_decode_attn_impl(impl if impl is not None else -1)
     try:
         case = make_case("cuda", ctx_list, L, H, HQ, D, seed=seed, pad_to=pad_to)
         out, _ = launch(case, layer, max_ctx=max_ctx)

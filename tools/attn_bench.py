@@ -32,13 +32,19 @@ def peak():
     return json.loads(p.read_text()).get("hbm_gbs", 6650.0) if p.exists() else 6650.0
 
 
+LAYOUT = "random"
+
+
 def run_case(pool, B, ctxs, plan_ctx, hq=32, reps=20, stream=None):
     dev = pool.device
     H, D = pool.H, pool.D
     nlb = (max(plan_ctx, max(ctxs)) + 15) // 16
     rng = np.random.default_rng(B * 7 + len(ctxs))
     need = [(c + 15) // 16 for c in ctxs]
-    perm = rng.permutation(pool.n_blocks)[: sum(need)].astype(np.int32)
+    if LAYOUT == "contig":  # every request's blocks consecutive (TLB / DRAM-page locality probe)
+        perm = np.arange(sum(need), dtype=np.int32)
+    else:
+        perm = rng.permutation(pool.n_blocks)[: sum(need)].astype(np.int32)
     tab = np.zeros((B, nlb), np.int32)
     o = 0
     for i, n in enumerate(need):  # distinct blocks for every context block (no L2 reuse)
@@ -81,10 +87,14 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--batches", default="32,64,96,128")
     ap.add_argument("--plans", default="exact,pool")
-    ap.add_argument("--impls", default="5", help="comma list of implementations (tf_paged_decode_attn_impl)")
+    ap.add_argument("--impls", default="0,3,5", help="comma list of implementations (tf_paged_decode_attn_impl)")
+    ap.add_argument("--layout", default="random", choices=["random", "contig"])
+    ap.add_argument("--pool-blocks", type=int, default=22000)
     args = ap.parse_args()
+    global LAYOUT
+    LAYOUT = args.layout
     dev = torch.device("cuda")
-    pool = KvPool(22000, 1, 32, 8, 128, device=dev)
+    pool = KvPool(args.pool_blocks, 1, 32, 8, 128, device=dev)
     pool.gpu.view(torch.bfloat16).normal_(0, 1)
     pk = peak()
     rng = np.random.default_rng(0)
