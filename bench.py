@@ -183,8 +183,11 @@ def run_ours(args):
             lockstep = Lockstep(dist.new_group(backend="gloo"))
         c2 = configs.c4(world)
         tr = _trace_for_rank(0, 1, args.arrivals)
-        if world > 1 and args.graphs:
-            args.graphs = 0  # eager decode under TP: NCCL all-reduces are not captured in graphs
+        if world > 1 and args.graphs and one_gpu:
+            # the one-GPU dry run carries the all-reduces over gloo, which cannot
+            # be captured; over NCCL (the real C4 run) the decode forward WITH its
+            # all-reduces is captured per bucket like the TP=1 one
+            args.graphs = 0
     else:
         c2 = configs.C2
         tr = _trace_for_rank(rank, world, args.arrivals)
@@ -205,7 +208,12 @@ def run_ours(args):
     if args.graphs:
         dp.enable_scratch()
         model.enable_graphs(dp)
-    policy = BufferAwarePolicy(c2.sched_cfg(SchedulerConfig))
+    if args.policy == "fcfs":  # the paper's comparison baseline on the same data plane
+        from paper_2510_02758_b200.scheduler import FcfsPolicy
+
+        policy = FcfsPolicy(c2.sched_cfg(SchedulerConfig))
+    else:
+        policy = BufferAwarePolicy(c2.sched_cfg(SchedulerConfig))
     tick_dump = []
     if args.dump_ticks:
         import dataclasses
@@ -251,23 +259,21 @@ def run_ours(args):
         live = sorted(r for r in eng.running if eng.state[r].status == "running")[: c2.max_batch]
         if not live:
             return
-        per = model.measure_attention(dp, live, [eng.state[r].kv.total_kv - 1 for r in live])
+        plan = "graph" if args.graphs else "exact"
+        per = model.measure_attention(dp, live, [eng.state[r].kv.total_kv - 1 for r in live], plan=plan)
         avg_ms = sum(ms for _, ms in per) / len(per)
         avg_bytes = sum(b for b, _ in per) / len(per)
         ach = avg_bytes / (avg_ms / 1e3) / 1e9
-        G = shape.n_q_heads // shape.n_kv_heads
-        kname = {"1": "paged_attn_kernel (v1)", "2": "paged_attn_tma_kernel (v2)",
-                 "3": f"paged_attn_mma_kernel<{G}> (v3) + combine"}.get(
-            os.environ.get("TF_ATTN_IMPL", "3")[:1], f"paged_attn_stream_kernel<{G}> (v4 stream-K, tensor cores)")
         traffic, tsrc = _ncu_traffic(avg_bytes)
-        state["roof"] = {"bound": "hbm", "kernel": kname, "achieved": round(ach, 1),
-                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4),
-                         "traffic": traffic, "traffic_source": tsrc,
-                         "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live),
+        state["roof"] = {"bound": "hbm", "kernel": _attn_kernel_name(shape, len(live), bool(args.graphs)),
+                         "achieved": round(ach, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(ach / hbm, 4), "traffic": traffic, "traffic_source": tsrc,
+                         "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live), "plan": plan,
                          "algorithmic_bytes_per_launch": round(avg_bytes),
                          "note": f"bytes = sum(ctx) x {pool.H * pool.D * 4} B (K+V, {pool.H} kv heads x {pool.D} x "
-                                 "bf16) + q/out + table entries per layer; re-launched right after the window on "
-                                 "the running batch"}
+                                 "bf16) + q/out + table entries per layer (real rows only); re-launched right after "
+                                 "the window on the running batch with the plan the decode graphs replay (batch "
+                                 "padded to its bucket with scratch rows, max_ctx = the pool maximum)"}
         if args.graphs:
             xf = dp.transfer_log()[state["ev0"]:state["ev1"]]
             per_step = lambda k: math.ceil(sum(n for d, n, _ in xf if d == k) / 16 / len(timed))  # noqa: E731
@@ -275,9 +281,18 @@ def run_ours(args):
             # blocks per direction that keep a ~55 GB/s link busy for one decode step
             sat = max(1, int(55e9 * (hid_w["t_decode_ms"] if hid_w else 7.0) / 1e3 / dp.pool.block_bytes))
             hid_s = measure_hidden(model, dp, eng, live, sat, sat)
-            state["hidden"] = {"window_volume": hid_w, "link_saturating": hid_s,
+            hid_m = measure_hidden_mix(model, dp, eng, live, state["ev0"], state["ev1"], len(timed),
+                                       args.swap_engine)
+            state["hidden"] = {"window_mix": hid_m, "window_volume": hid_w, "link_saturating": hid_s,
                                "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = the captured forward of "
-                                       "the live batch; swaps on copy engines, own streams"}
+                                       "the live batch; window_mix replays the window's own chunks (their segment "
+                                       "shapes, the serving engine) per step; window_volume / link_saturating move "
+                                       "whole blocks on the copy engines"}
+        if not args.no_selector:
+            sys.path.insert(0, str(ROOT / "tools"))
+            from selector_latency import gpu_selector_latency
+
+            state["selector_gpu"] = gpu_selector_latency()
 
     def on_step(rec, eng):
         n = len(eng.steps)
@@ -303,6 +318,7 @@ def run_ours(args):
                 state["pre1"], state["rc1"] = eng.total_preemptions, eng.total_recomputes
                 state["launch1"] = model.launch_count()
                 state["phase"] = "done"
+                state["h2d_launch_at_end"] = dp.stats["h2d_launches"]
                 torch.cuda.nvtx.range_pop()
                 t_p = time.perf_counter()
                 window_probes(eng, state["timed"])
@@ -313,9 +329,33 @@ def run_ours(args):
                 else:
                     eng._stop = True
             return
+        if state["phase"] in ("ttft", "rest") and args.swap_steps > 0:
+            # swap-phase sub-window: the next --swap-steps decode steps after the
+            # first load (h2d chunk) issued once the main window ended - so even
+            # a short main window from t=0 (decode + write-through only) comes
+            # with measured evict / load traffic from the same run
+            sw = state.setdefault("sw", {"phase": "wait"})
+            if sw["phase"] == "wait" and dp.stats["h2d_launches"] > state["h2d_launch_at_end"]:
+                sw.update(phase="on", ev0=len(dp._events), pre0=eng.total_preemptions, rc0=eng.total_recomputes,
+                          steps=[], wall0=time.perf_counter())
+            elif sw["phase"] == "on":
+                sw["steps"].append(dict(rec))
+                if len(sw["steps"]) >= args.swap_steps:
+                    sw.update(phase="done", ev1=len(dp._events), pre1=eng.total_preemptions,
+                              rc1=eng.total_recomputes, wall1=time.perf_counter())
+                    if args.graphs:
+                        t_p = time.perf_counter()
+                        torch.cuda.synchronize()
+                        live = sorted(r for r in eng.running if eng.state[r].status == "running")[: c2.max_batch]
+                        if live:
+                            sw["hidden"] = measure_hidden_mix(model, dp, eng, live, sw["ev0"], sw["ev1"],
+                                                              len(sw["steps"]), args.swap_engine)
+                        eng.shift_clock(time.perf_counter() - t_p)
         if state["phase"] == "ttft" and all(st.record.gen_times for st in eng.state.values()):
-            state["ttft_done_at"] = eng.now
-            eng._stop = True
+            sw = state.get("sw", {"phase": "done"})
+            if sw["phase"] == "done" or args.swap_steps <= 0 or (sw["phase"] == "wait" and not eng.h2d.queue):
+                state["ttft_done_at"] = eng.now
+                eng._stop = True
 
     eng = RealtimeEngine(tr, policy, cm, sim, dp, skip_idle=True, on_step=on_step, lockstep=lockstep,
                          max_wall_s=args.max_wall if args.full_run else None)
@@ -333,54 +373,41 @@ def run_ours(args):
     if state["phase"] not in ("done", "ttft", "rest"):
         raise RuntimeError(f"bench ended in phase {state['phase']} after {len(eng.steps)} steps")
     timed = state["timed"]
-    # device time of the window: every GPU job (decode iterations and the
-    # prefill / recompute jobs interleaved with them) that ran inside it
-    t_lo, t_hi = timed[0]["start"], timed[-1]["end"]
-    win_jobs = [j for j in eng.jobs if t_lo <= j[1] and j[2] <= t_hi]
-    dev_s = sum(j[3] for j in win_jobs)
-    prefill_s = sum(j[3] for j in win_jobs if j[0] == "prefill")
-    eff = sum(s["effective"] for s in timed)
-    toks = sum(s["tokens"] for s in timed)
-    wall = state["wall1"] - state["wall0"]
-    dev_s = _max_over_ranks(dev_s, world, dev)
-    wall = _max_over_ranks(wall, world, dev)
-    if not tp_mode:  # replicas: every rank generated its own tokens
-        eff = _sum_over_ranks(eff, world, dev)
-        toks = _sum_over_ranks(toks, world, dev)
-    # swap traffic of the window (bytes per token = all layers' K and V of this rank's shard)
-    bpt = shape.kv_bytes_per_token // tp_size
-    xfers = dp.transfer_log()[state["ev0"]:state["ev1"]]
-    d2h_tok = sum(n for k, n, _ in xfers if k == "d2h")
-    h2d_tok = sum(n for k, n, _ in xfers if k == "h2d")
-    d2h_ms = sum(ms for k, _, ms in xfers if k == "d2h")
-    h2d_ms = sum(ms for k, _, ms in xfers if k == "h2d")
-    if world > 1 and not tp_mode:  # C3: every replica's own link, rates over all replicas' chunks
-        d2h_tok, h2d_tok = int(_sum_over_ranks(d2h_tok, world, dev)), int(_sum_over_ranks(h2d_tok, world, dev))
-        d2h_ms, h2d_ms = _sum_over_ranks(d2h_ms, world, dev), _sum_over_ranks(h2d_ms, world, dev)
-    swap = {"d2h_tokens": d2h_tok, "h2d_tokens": h2d_tok, "chunks": len(xfers),
-            "engine": {0: "SM kernel", 1: "copy-engine batch", 2: "auto (CE whole blocks + SM partial)"}[
-                args.swap_engine],
-            "d2h_gbs": (d2h_tok * bpt / (d2h_ms / 1e3) / 1e9) if d2h_ms else None,
-            "h2d_gbs": (h2d_tok * bpt / (h2d_ms / 1e3) / 1e9) if h2d_ms else None,
-            "pcie_gen5_gbs": PCIE_GEN5_GBS,
-            "preemptions": state["pre1"] - state["pre0"], "recomputes": state["rc1"] - state["rc0"]}
-    for k in ("d2h", "h2d"):
-        if swap[f"{k}_gbs"]:
-            swap[f"{k}_frac_pcie"] = swap[f"{k}_gbs"] / PCIE_GEN5_GBS
-    roof = state.get("roof")
+    bpt = shape.kv_bytes_per_token // tp_size  # swap bytes per token: all layers' K and V of this rank's shard
+    local = _window_stats(eng, dp, timed, state["ev0"], state["ev1"], bpt)
+    local.update(ttft_lat=[r.gen_times[0] - r.arrival for r in res.records if r.gen_times],
+                 n_records=len(res.records), preemptions=state["pre1"] - state["pre0"],
+                 recomputes=state["rc1"] - state["rc0"], wall=state["wall1"] - state["wall0"])
+    red_dev = torch.device("cpu") if (world > 1 and one_gpu) else dev
+    agg = _aggregate(local, world, tp_mode, red_dev)
+    sw = state.get("sw")
+    sw_out = None
+    if sw and sw.get("steps"):
+        sl = _window_stats(eng, dp, sw["steps"], sw["ev0"], sw.get("ev1", len(dp._events)), bpt)
+        sl.update(ttft_lat=[], n_records=0, preemptions=sw.get("pre1", eng.total_preemptions) - sw["pre0"],
+                  recomputes=sw.get("rc1", eng.total_recomputes) - sw["rc0"],
+                  wall=sw.get("wall1", time.perf_counter()) - sw["wall0"])
+        sa = _aggregate(sl, 1, tp_mode, red_dev)  # rank-local (each replica's own window)
+        sw_out = {"steps": len(sw["steps"]), "complete": sw["phase"] == "done",
+                  "value": sa["value"], "e2e_value": sa["e2e"], "swap": _swap_block(sa, args.swap_engine),
+                  "preemptions": sl["preemptions"], "recomputes": sl["recomputes"],
+                  "hidden_under_decode": sw.get("hidden"),
+                  "note": f"the {args.swap_steps} decode steps after the first load (h2d chunk) issued once the main "
+                          "window ended (rank 0's replica); value = effective tokens / device time, e2e = / host wall"}
+    swap = _swap_block(agg, args.swap_engine)
+    swap.update(preemptions=local["preemptions"], recomputes=local["recomputes"])
     if state.get("hidden"):
         swap["hidden_under_decode"] = state["hidden"]
-    ttft = [r for r in res.records if r.gen_times]
     out = {
         "metric": METRIC,
-        "value": eff / dev_s if dev_s > 0 else None,
+        "value": agg["value"],
         "unit": "effective tok/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": dev_s / len(timed) * 1e3,
-        "decode_ms_per_step": sum(s["dur"] for s in timed) / len(timed) * 1e3,
-        "prefill_device_s_in_window": round(prefill_s, 4),
+        "ms_per_step": agg["dev_s"] / len(timed) * 1e3,
+        "decode_ms_per_step": sum(st_["dur"] for st_ in timed) / len(timed) * 1e3,
+        "prefill_device_s_in_window": round(local["prefill_s"], 4),
         "higher_is_better": True,
         "scaling": "strong" if tp_mode else "weak",
         "vs_baseline": None,
@@ -393,29 +420,35 @@ def run_ours(args):
                                (f"C2: Llama3-8B bf16 random-init, 1xB200 per replica, 256-request {args.arrivals} "
                                 "(bodies of the first 256 arrivals of the lambda=10/s 30 s trace, seed 1), KV pool "
                                 "163,840 tokens (20 GiB) + pinned host tier, block 16, max_batch 128"),
-                   "model": shape.name, "global_batch": max(s["batch"] for s in timed),
-                   "mean_batch": round(statistics.mean(s["batch"] for s in timed), 1),
+                   "model": shape.name, "global_batch": max(st_["batch"] for st_ in timed),
+                   "mean_batch": round(statistics.mean(st_["batch"] for st_ in timed), 1),
                    "seq_len": None, "parallelism": f"tp{world}" if tp_mode else f"replicas x{world}",
-                   "arrivals": args.arrivals,
+                   "policy": policy.name, "arrivals": args.arrivals,
                    "l2": "working set (weights + KV, tens of GB) >> 126 MB L2; no flush needed",
                    "timed_region": f"decode iterations [{args.warmup}, {args.warmup + args.steps}) from t=0 "
                                    "of the real-time loop (measured clock, idle gaps skipped)",
                    "cuda_graphs": bool(args.graphs), "fused_write_through": bool(args.fused_wt)},
-        "raw_tok_s": toks / dev_s if dev_s > 0 else None,
-        "e2e": {"value": eff / wall if wall > 0 else None, "unit": "effective tok/s",
-                "h2d_bytes_per_step": int((h2d_tok * bpt + sum(s["batch"] for s in timed) * 24) / len(timed)),
-                "d2h_bytes_per_step": int((d2h_tok * bpt + sum(s["batch"] for s in timed) * 8) / len(timed))},
+        "raw_tok_s": agg["raw"],
+        "e2e": {"value": agg["e2e"], "unit": "effective tok/s",
+                "h2d_bytes_per_step": int((agg["h2d_tok"] * bpt + local["batch_sum"] * 24) / len(timed)),
+                "d2h_bytes_per_step": int((agg["d2h_tok"] * bpt + local["batch_sum"] * 8) / len(timed))},
         "swap": swap,
-        "roofline": roof,
+        "swap_window": sw_out,
+        "roofline": state.get("roof"),
         "clocks": sampler.summary(),
-        "gpu_launches": None,
-        "first_tokens_in_window": len(ttft),
-        "ttft": _ttft_summary(ttft, len(res.records), world, tp_mode),
+        "gpu_launches": int(state["launch1"] - state["launch0"]),
+        "first_tokens_in_window": len(local["ttft_lat"]),
+        "ttft": agg["ttft"],
     }
-    # this library's kernel launches inside the window, counted: every C-ABI
-    # launch increments a counter in the .so, and each graph replay adds the
-    # number of the library's kernels captured in that graph
-    out["gpu_launches"] = int(state["launch1"] - state["launch0"])
+    # gpu_launches: this library's kernel launches inside the window, counted:
+    # every C-ABI launch increments a counter in the .so, and each graph replay
+    # adds the number of the library's kernels captured in that graph
+    if state.get("selector_gpu"):
+        out["selector"] = {"gpu": state["selector_gpu"],
+                           "note": "us per call at N members: e2e = host wall (pack, H2D, one single-CTA launch, "
+                                   "D2H, unpack), device = CUDA events around the call on the selector's stream; "
+                                   "launch_floor = an empty kernel (tf_launch_floor); the CPU reference (oracle "
+                                   "restatement of tokensim on_tick / select_batch, 1 core) is in cpu_baseline"}
     if args.full_run:
         from paper_2510_02758_b200.metrics import EffectiveThroughputConfig, effective_throughput
 
@@ -440,6 +473,8 @@ def run_ours(args):
             json.dump({"ticks": tick_dump, "decision_log": res.decision_log}, f)
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, timed, quick=True)
+        if out.get("selector") and out["cpu_baseline"].get("selector_cpu"):
+            out["selector"]["cpu_oracle_1core"] = out["cpu_baseline"]["selector_cpu"]
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
@@ -449,12 +484,78 @@ def run_ours(args):
     return out
 
 
-def _ttft_summary(recs, n_records, world, tp_mode):
+def _window_stats(eng, dp, steps, ev0, ev1, bpt):
+    """This rank's numbers for a window of decode steps: device time of every
+    GPU job inside it (decode iterations and the prefills between them),
+    effective / raw tokens, and the window's swap chunks (tokens, CUDA-event ms)."""
+    t_lo, t_hi = steps[0]["start"], steps[-1]["end"]
+    win_jobs = [j for j in eng.jobs if t_lo <= j[1] and j[2] <= t_hi]
+    xf = dp.transfer_log()[ev0:ev1]
+    return {"dev_s": sum(j[3] for j in win_jobs), "prefill_s": sum(j[3] for j in win_jobs if j[0] == "prefill"),
+            "eff": sum(st_["effective"] for st_ in steps), "toks": sum(st_["tokens"] for st_ in steps),
+            "batch_sum": sum(st_["batch"] for st_ in steps),
+            "d2h_tok": sum(n for k, n, _ in xf if k == "d2h"), "h2d_tok": sum(n for k, n, _ in xf if k == "h2d"),
+            "d2h_ms": sum(ms for k, _, ms in xf if k == "d2h"), "h2d_ms": sum(ms for k, _, ms in xf if k == "h2d"),
+            "chunks": len(xf), "bpt": bpt}
+
+
+def _aggregate(local, world, tp_mode, device):
+    """Whole-job numbers from every rank's window stats.  Replicas (C2/C3):
+    tokens and swap traffic are summed (each replica serves its own requests
+    over its own link), device time and wall time are the max over ranks, and
+    TTFT latencies are gathered from every rank.  Tensor parallel (C4): every
+    rank serves the same tokens in lockstep, so rank 0's counts stand and the
+    times are still the max over ranks."""
+    dev_s = _max_over_ranks(local["dev_s"], world, device)
+    wall = _max_over_ranks(local["wall"], world, device)
+    eff, toks = local["eff"], local["toks"]
+    d2h_tok, h2d_tok, d2h_ms, h2d_ms = local["d2h_tok"], local["h2d_tok"], local["d2h_ms"], local["h2d_ms"]
+    if not tp_mode:
+        eff, toks = _sum_over_ranks(eff, world, device), _sum_over_ranks(toks, world, device)
+        if world > 1:
+            d2h_tok, h2d_tok = int(_sum_over_ranks(d2h_tok, world, device)), int(_sum_over_ranks(h2d_tok, world, device))
+            d2h_ms, h2d_ms = _sum_over_ranks(d2h_ms, world, device), _sum_over_ranks(h2d_ms, world, device)
+    bpt = local["bpt"]
+    return {"dev_s": dev_s, "wall": wall, "eff": eff, "toks": toks,
+            "value": eff / dev_s if dev_s > 0 else None, "raw": toks / dev_s if dev_s > 0 else None,
+            "e2e": eff / wall if wall > 0 else None,
+            "d2h_tok": d2h_tok, "h2d_tok": h2d_tok, "chunks": local["chunks"],
+            "d2h_gbs": (d2h_tok * bpt / (d2h_ms / 1e3) / 1e9) if d2h_ms else None,
+            "h2d_gbs": (h2d_tok * bpt / (h2d_ms / 1e3) / 1e9) if h2d_ms else None,
+            "ttft": _ttft_summary_lat(local["ttft_lat"], local["n_records"], world, tp_mode)}
+
+
+def _swap_block(agg, engine):
+    sw = {"d2h_tokens": agg["d2h_tok"], "h2d_tokens": agg["h2d_tok"], "chunks": agg["chunks"],
+          "engine": {0: "SM kernel", 1: "copy-engine batch (1-D runs)",
+                     2: "copy engines (whole blocks batched, partial blocks as 2-D copies)",
+                     3: "copy engines (whole blocks batched, partial blocks as 2-D copies)"}[engine],
+          "d2h_gbs": agg["d2h_gbs"], "h2d_gbs": agg["h2d_gbs"], "pcie_gen5_gbs": PCIE_GEN5_GBS}
+    for k in ("d2h", "h2d"):
+        if sw[f"{k}_gbs"]:
+            sw[f"{k}_frac_pcie"] = sw[f"{k}_gbs"] / PCIE_GEN5_GBS
+    return sw
+
+
+def _attn_kernel_name(shape, batch, graphs):
+    """The decode-attention implementation the library picks for this launch
+    (tf_paged_decode_attn_impl default: v5 for B <= 64, v3 above)."""
+    G = shape.n_q_heads // shape.n_kv_heads
+    env = os.environ.get("TF_ATTN_IMPL", "")[:1]
+    impl = int(env) if env in ("1", "2", "3", "4", "5") else 0
+    if impl == 0:
+        impl = 5 if batch <= 64 else 3
+    return {1: "paged_attn_kernel (v1, CUDA cores)", 2: "paged_attn_tma_kernel (v2, bulk copy)",
+            3: f"paged_attn_mma_kernel<{G}> (v3, split-KV cp.async + mma.sync) + combine",
+            4: f"paged_attn_stream_kernel<{G}> (v4 stream-K)",
+            5: f"paged_attn_tma5_kernel<{G}> (v5, TMA tensor loads + stream-K)"}[impl]
+
+
+def _ttft_summary_lat(lat, n_records, world, tp_mode):
     """TTFT latency stats (first token - arrival, nearest-rank P99,
     tokensim/metrics.py:144-155) over ALL replicas' requests (C3: gathered)."""
     from paper_2510_02758_b200.metrics import nearest_rank
 
-    lat = [r.gen_times[0] - r.arrival for r in recs]
     total = n_records
     if world > 1 and not tp_mode:
         import torch.distributed as dist
@@ -471,6 +572,10 @@ def _ttft_summary(recs, n_records, world, tp_mode):
             "note": "TTFT latency = first token - arrival (nearest-rank P99, tokensim/metrics.py:144-155)" + (
                 ", real-time serving continued after the window until every request had its first token"
                 if len(v) == total else ", requests that had their first token by the end of the run")}
+
+
+def _ttft_summary(recs, n_records, world, tp_mode):
+    return _ttft_summary_lat([r.gen_times[0] - r.arrival for r in recs], n_records, world, tp_mode)
 
 
 def _ncu_traffic(alg_bytes):
@@ -585,32 +690,174 @@ def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=24):
             "method": "median of 5 alternating rounds of 24 steps each (decode alone / both / swaps alone)"}
 
 
-def cpu_baseline(args, timed, quick=False):
-    """The oracle's CPU restatement of one decode step of the same batch shape."""
-    from oracle.cpu_baseline import time_cpu_step
+def measure_hidden_mix(model, dp, eng, rids, ev0, ev1, nsteps, engine, steps=24):
+    """Transfer hidden under decode for the window's OWN swap mix: the chunks
+    the engine issued in the window (their segment shapes, one call per chunk,
+    the serving engine), spread at the window's per-step density over
+    ``steps`` decode steps of the captured forward of the live batch, alone /
+    with the swaps / swaps alone.  Scratch blocks stand in for the live ones
+    (same shapes, no live KV touched)."""
+    import ctypes as C
 
-    b = max(1, int(statistics.median([s["batch"] for s in timed])) if timed else 32)
-    return time_cpu_step(batch=b, ctx=2600, threads=os.cpu_count() or 1, seconds=args.cpu_seconds)
+    import torch
+
+    from paper_2510_02758_b200 import _lib
+
+    chunks = [(dp._events[i][0], dp._seglog[i]) for i in range(ev0, min(ev1, len(dp._seglog)))]
+    if not chunks or nsteps <= 0:
+        return None
+    per_step = len(chunks) / nsteps
+    take = chunks[: max(1, round(per_step * steps))]
+    nseg = max(len(sg) for _, sg in take)
+    pool = dp.pool
+    k = min(64, nseg * 4)
+    if pool.free_count(_lib.TIER_GPU) < k or pool.free_count(_lib.TIER_HOST) < k:
+        return None
+    g = pool.alloc(_lib.TIER_GPU, k)
+    h = pool.alloc(_lib.TIER_HOST, k)
+    calls, j = [[] for _ in range(steps)], 0
+    for i, (kind, sg) in enumerate(take):
+        arr = dp._seg_array([(g[(j + t) % k], h[(j + t) % k], s0, n) for t, (s0, n) in enumerate(sg)])
+        j += len(sg)
+        calls[min(steps - 1, int(i / per_step))].append((kind, arr, len(sg)))
+    pos = [eng.state[r].kv.total_kv - 1 for r in rids]
+    st = dp.s_compute
+
+    def decode():
+        with torch.cuda.stream(st):
+            model._decode_graph(dp, rids, pos, st)
+
+    def swaps(si):
+        for kind, arr, n in calls[si]:
+            fn = _lib.lib.tf_kv_gather_d2h if kind == "d2h" else _lib.lib.tf_kv_scatter_h2d
+            stream = dp.s_evict if kind == "d2h" else dp.s_load
+            _lib.check(fn(pool.handle, arr, n, 0, pool.L, engine, C.c_void_p(stream.cuda_stream)))
+
+    def run(dec, swp):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for si in range(steps):
+            if dec:
+                decode()
+            if swp:
+                swaps(si)
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / steps
+
+    decode()
+    swaps(0)
+    rounds = {"dec": [], "swp": [], "both": []}
+    for _ in range(5):
+        rounds["dec"].append(run(True, False))
+        rounds["both"].append(run(True, True))
+        rounds["swp"].append(run(False, True))
+    t_dec, t_swp, t_both = (statistics.median(rounds[x]) for x in ("dec", "swp", "both"))
+    pool.free(_lib.TIER_GPU, g)
+    pool.free(_lib.TIER_HOST, h)
+    toks = sum(n for _, sg in take for _, n in sg)
+    return {"chunks_per_step": round(per_step, 2), "tokens_per_step": round(toks / steps, 1), "batch": len(rids),
+            "t_decode_ms": round(t_dec * 1e3, 3), "t_swap_ms": round(t_swp * 1e3, 3),
+            "t_both_ms": round(t_both * 1e3, 3),
+            "hidden_frac": round(min(1.0, 1.0 - max(0.0, t_both - t_dec) / t_swp), 4) if t_swp > 0 else None,
+            "method": "the window's chunks replayed at its per-step density; median of 5 alternating rounds of "
+                      f"{steps} steps (decode alone / both / swaps alone)"}
+
+
+def cpu_baseline(args, timed, quick=False):
+    """CPU baseline (reported beside the GPU numbers),
+    all of it the oracle's restatement of the reference on the host:
+    one C2 decode step of the window's median batch (all host cores), the
+    reference simulator on the same C2 burst (1 core, per-call on_tick /
+    plan_write_chunk / _snapshot), the policy's on_tick / select_batch at the
+    selector's N, and the host's CPU model / NUMA layout."""
+    from oracle.cpu_baseline import host_info, time_cpu_step, time_reference_sim
+
+    b = max(1, int(statistics.median([s["batch"] for s in timed])) if timed else 128)
+    out = time_cpu_step(batch=b, ctx=2600, threads=os.cpu_count() or 1, seconds=args.cpu_seconds)
+    out["reference_sim"] = time_reference_sim("c2_burst256_s1_tokenflow")
+    out["host"] = host_info()
+    if not args.no_selector:
+        sys.path.insert(0, str(ROOT / "tools"))
+        from selector_latency import cpu_selector_latency
+
+        out["selector_cpu"] = cpu_selector_latency()
+    return out
 
 
 def run_reference(args):
     world, rank, _ = _dist()
     if rank != 0:
         return None
-    from oracle.cpu_baseline import time_cpu_step
+    from oracle.cpu_baseline import host_info, time_cpu_step, time_reference_sim
 
     cb = time_cpu_step(batch=args.ref_batch, ctx=2600, threads=os.cpu_count() or 1, seconds=args.cpu_seconds)
-    out = {"metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-           "data": "synthetic", "impl": "reference",
+    cb["reference_sim"] = time_reference_sim("c2_burst256_s1_tokenflow")
+    cb["host"] = host_info()
+    out = {"metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": max(world, args.gpus),
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "impl": "reference",
            "config": {"workload": "C2: Llama3-8B bf16 random-init, 256-request burst (the same population and "
                                   "metric as the ours arm); the reference's CPU path = the oracle restatement of one "
-                                  "decode step of the C2 batch on the host cores (tokensim itself has no tensors)",
-                      "model": "llama3-8b", "parallelism": "host CPU"},
+                                  f"decode step at B={args.ref_batch} (the burst's opening decode batch = the ours "
+                                  "arm's window batch from t=0) on the host cores (tokensim itself has no tensors)",
+                      "model": "llama3-8b", "parallelism": "host CPU", "global_batch": args.ref_batch},
            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
                                        "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     return out
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing without a GPU (gloo on the CPU):
+    every rank fabricates deterministic window stats, and the SAME aggregation
+    and reporting path as a real run turns them into the line (CPU tests of
+    --gpus N self-launch and the C3 aggregation)."""
+    import torch
+
+    world, rank, _ = _dist()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+    tp_mode = args.config == "c4"
+    local = {"dev_s": 1.0 + 0.25 * rank, "prefill_s": 0.0, "eff": 100.0 * (rank + 1), "toks": 120.0 * (rank + 1),
+             "batch_sum": 10, "d2h_tok": 1000 * (rank + 1), "h2d_tok": 500, "d2h_ms": 10.0, "h2d_ms": 5.0,
+             "chunks": 7, "bpt": 131072, "ttft_lat": [float(rank) + i / 10 for i in range(10)], "n_records": 10,
+             "wall": 2.0 + rank}
+    agg = _aggregate(local, world, tp_mode, torch.device("cpu"))
+    out = {"metric": METRIC, "value": agg["value"], "unit": "effective tok/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+           "scaling": "strong" if tp_mode else "weak", "data": "dry-run (no GPU work; fabricated per-rank stats)",
+           "config": {"parallelism": f"tp{world}" if tp_mode else f"replicas x{world}"},
+           "e2e": {"value": agg["e2e"]}, "swap": _swap_block(agg, args.swap_engine), "ttft": agg["ttft"]}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return out
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _self_launch(args) -> bool:
+    """``--gpus N`` without a launcher: re-run this script under
+    torch.distributed.run with one rank per GPU (127.0.0.1 rendezvous); rank 0
+    prints the single aggregated line.  Under torchrun (WORLD_SIZE set) the
+    ranks are already there."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    rc = subprocess.call(cmd)
+    raise SystemExit(rc)
 
 
 def main():
@@ -622,8 +869,8 @@ def main():
     # pinned host tier: 16384 x 2 MiB = 32 GiB covers the timed window; a
     # full run of the burst peaks near 22K blocks (replay of the same trace)
     ap.add_argument("--host-blocks", type=int, default=int(os.environ.get("TF_HOST_BLOCKS", 0)))
-    ap.add_argument("--swap-engine", type=int, default=2, help="0 SM kernel, 1 copy engines, 2 auto (whole "
-                    "blocks on copy engines, partial blocks on the SM kernel)")
+    ap.add_argument("--swap-engine", type=int, default=2, help="0 SM kernel, 1 copy engines (1-D runs), 2 copy "
+                    "engines (whole blocks batched, each partial block one 2-D copy)")
     ap.add_argument("--arrivals", default="burst", choices=["burst", "poisson"])
     ap.add_argument("--config", default="c2", choices=["c2", "c4"], help="c2: Llama3-8B replicas (C2/C3, default); "
                     "c4: Qwen2.5-32B tensor-parallel over the launched ranks")
@@ -637,8 +884,15 @@ def main():
                     "its first token (complete P99 TTFT of the burst); default on for c2, off for c4")
     ap.add_argument("--max-wall", type=float, default=600.0, help="--full-run: stop (truncated) after this many "
                     "seconds of wall time")
-    ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    ap.add_argument("--ref-batch", type=int, default=64)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-batch", type=int, default=128, help="reference arm: the decode batch of the timed "
+                    "window (the C2 burst runs at max_batch=128 from t=0)")
+    ap.add_argument("--policy", default="tokenflow", choices=["tokenflow", "fcfs"], help="fcfs: the paper's "
+                    "comparison baseline (tokensim/scheduler.py:828-880) on the same B200 data plane")
+    ap.add_argument("--swap-steps", type=int, default=200, help="swap-phase sub-window: decode steps after the first "
+                    "load issued once the main window ended (0: off)")
+    ap.add_argument("--no-selector", action="store_true", help="skip the selector latency block")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (no GPU work; CPU tests)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--watchdog", type=float, default=0.0, help="debug: dump engine state every N seconds")
@@ -663,7 +917,10 @@ def main():
             pass
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    if args.impl == "reference":
+    _self_launch(args)
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -171,14 +171,16 @@ def wt_chunks(pool, args):
         arr = (_lib.TfSeg * len(segs))()
         for i, (g, h, s0, k) in enumerate(segs):
             arr[i].gpu_block, arr[i].host_block, arr[i].slot_begin, arr[i].n_slots = g, h, s0, k
-        for eng in (0, 1, 2):
-            def go():
-                _lib.check(_lib.lib.tf_kv_gather_d2h(pool.handle, arr, len(segs), 0, pool.L, eng,
-                                                     C.c_void_p(st.cuda_stream)))
-            t = timed(go, st, reps=20)
-            rows.append({"tokens": n, "engine": {0: "sm", 1: "ce", 2: "auto"}[eng], "segments": len(segs),
-                         "us": round(t * 1e6, 2), "gbs": round(n * bpt / t / 1e9, 2)})
-            print(json.dumps(rows[-1]), flush=True)
+        for eng in (0, 1, 2, 3):
+            for d in ("d2h", "h2d"):
+                fn = _lib.lib.tf_kv_gather_d2h if d == "d2h" else _lib.lib.tf_kv_scatter_h2d
+
+                def go(fn=fn, eng=eng):
+                    _lib.check(fn(pool.handle, arr, len(segs), 0, pool.L, eng, C.c_void_p(st.cuda_stream)))
+                t = timed(go, st, reps=20)
+                rows.append({"tokens": n, "dir": d, "engine": {0: "sm", 1: "ce", 2: "auto", 3: "ce2d"}[eng],
+                             "segments": len(segs), "us": round(t * 1e6, 2), "gbs": round(n * bpt / t / 1e9, 2)})
+                print(json.dumps(rows[-1]), flush=True)
     del first, dev
     return rows
 

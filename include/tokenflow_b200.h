@@ -50,13 +50,17 @@ extern "C" {
 #define TF_TIER_HOST 1
 #define TF_ENGINE_SM 0 /* SM-driven zero-copy gather/scatter kernel */
 #define TF_ENGINE_CE 1 /* copy engines (cudaMemcpyBatchAsync of contiguous runs) */
-#define TF_ENGINE_AUTO 2 /* whole blocks on copy engines, partial blocks on the SM kernel */
+#define TF_ENGINE_AUTO 2 /* = TF_ENGINE_CE2D (kept for callers of ABI v1) */
+#define TF_ENGINE_CE2D 3 /* copy engines only: whole blocks batched, each partial block one 2-D copy */
 
 const char* tf_last_error(void);
 int tf_abi_version(void);
 /* Kernel launches issued through this library so far (captured launches
  * count once, at capture - a graph replay re-runs them without calling in). */
 int64_t tf_launch_count(void);
+/* Launch one empty kernel on the stream: the launch-latency floor that the
+ * selector's per-tick latency is reported against. */
+int tf_launch_floor(void* stream);
 
 /* ------------------------------------------------------------------ pool --
  * Block-major KV layout shared by HBM pool and pinned host store:

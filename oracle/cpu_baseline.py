@@ -37,6 +37,73 @@ def _tick_seconds(reps=3) -> float:
     return (time.perf_counter() - t0) / len(views)
 
 
+def time_reference_sim(name: str = "c1_tokenflow") -> dict:
+    """the reference simulator (oracle restatement,
+    strictly sequential: 1 core) on a frozen golden run, with the per-call
+    cost of its hot-path functions measured inside that run: on_tick
+    (tokensim/scheduler.py:513-736), plan_write_chunk (tokensim/kvstore.py:
+    112-141, writeback_plan here) and _snapshot (tokensim/engine.py:993-1061).
+    The event hash is checked against the golden run (same work as the reference)."""
+    import oracle.refsim.sim as simmod
+    from oracle.refsim.planner import Costs
+    from oracle.refsim.policy import Knobs, build_policy
+    from oracle.refsim.sim import SimKnobs
+    from oracle.refsim.traces import read_trace
+
+    g = json.load(gzip.open(ROOT / "tests" / "golden" / "runs" / f"{name}.json.gz"))
+    reqs = read_trace(str(ROOT / "tests" / "golden" / "traces" / f"{g['trace']}.csv"))
+    acc = {"on_tick": [0, 0.0], "plan_write_chunk": [0, 0.0], "snapshot": [0, 0.0]}
+
+    def timed(key, fn):
+        def w(*a, **k):
+            t0 = time.perf_counter()
+            try:
+                return fn(*a, **k)
+            finally:
+                acc[key][0] += 1
+                acc[key][1] += time.perf_counter() - t0
+        return w
+
+    pol = build_policy(g["policy"], Knobs(**g["sched"]))
+    pol.on_tick = timed("on_tick", pol.on_tick)
+    orig_wb, orig_snap = simmod.writeback_plan, simmod.Sim.snapshot
+    simmod.writeback_plan = timed("plan_write_chunk", orig_wb)
+    simmod.Sim.snapshot = timed("snapshot", orig_snap)
+    try:
+        t0 = time.perf_counter()
+        out = simmod.Sim(reqs, pol, Costs(**g["cm"]), SimKnobs(**g["sim"])).run()
+        wall = time.perf_counter() - t0
+    finally:
+        simmod.writeback_plan, simmod.Sim.snapshot = orig_wb, orig_snap
+    return {"run": name, "requests": len(reqs), "wall_s": round(wall, 4), "cores": 1,
+            "event_hash_ok": out.event_hash() == g["event_hash"],
+            "per_call_us": {k: round(v[1] / v[0] * 1e6, 2) for k, v in acc.items() if v[0]},
+            "calls": {k: v[0] for k, v in acc.items()}}
+
+
+def host_info() -> dict:
+    """CPU model, core count and NUMA layout of the host."""
+    import os
+
+    info = {"nproc": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    nodes = []
+    base = Path("/sys/devices/system/node")
+    for d in sorted(base.glob("node[0-9]*")) if base.exists() else []:
+        try:
+            nodes.append({"node": d.name, "cpus": (d / "cpulist").read_text().strip()})
+        except OSError:
+            pass
+    info["numa_nodes"] = nodes
+    return info
+
+
 def time_cpu_step(batch: int = 64, ctx: int = 2600, threads: int = 16, seconds: float = 20.0,
                   swap_tokens_per_step: int = 64) -> dict:
     from paper_2510_02758_b200.configs import LLAMA3_8B as S
@@ -44,10 +111,15 @@ def time_cpu_step(batch: int = 64, ctx: int = 2600, threads: int = 16, seconds: 
     torch.set_num_threads(threads)
     d, hq, hkv, hd, ffn = S.hidden, S.n_q_heads, S.n_kv_heads, S.head_dim, S.ffn
     bf = torch.bfloat16
-    layers = [{k: torch.zeros(*sh, dtype=bf) for k, sh in (("wqkv", (d, (hq + 2 * hkv) * hd)), ("wo", (hq * hd, d)),
-                                                             ("wgu", (d, 2 * ffn)), ("wd", (ffn, d)))}
+    gen = torch.Generator().manual_seed(0)
+
+    def w(*sh):  # random-init N(0, 0.02) like the GPU arm's weights
+        return (torch.randn(*sh, generator=gen) * 0.02).to(bf)
+
+    layers = [{k: w(*sh) for k, sh in (("wqkv", (d, (hq + 2 * hkv) * hd)), ("wo", (hq * hd, d)),
+                                       ("wgu", (d, 2 * ffn)), ("wd", (ffn, d)))}
               for _ in range(L_SAMPLE)]
-    lm = torch.zeros(d, S.vocab, dtype=bf)
+    lm = w(d, S.vocab)
     kv = [torch.randn(batch, 2, hkv, ctx, hd, dtype=torch.float32) for _ in range(L_SAMPLE)]
     x0 = torch.randn(batch, d, dtype=bf)
 

@@ -15,7 +15,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_tf_b200.so"
 
 TF_OK, TF_EINVAL, TF_ENOMEM, TF_EIO = 0, -22, -12, -5
 TIER_GPU, TIER_HOST = 0, 1
-ENGINE_SM, ENGINE_CE, ENGINE_AUTO = 0, 1, 2
+ENGINE_SM, ENGINE_CE, ENGINE_AUTO, ENGINE_CE2D = 0, 1, 2, 3
 
 
 class InvariantError(AssertionError):
@@ -119,6 +119,7 @@ SIGNATURES = {
     "tf_kv_scatter_h2d": (C.c_int, [_I64, C.POINTER(TfSeg), _I32, _I32, _I32, _I32, _P]),
     "tf_copy_small": (C.c_int, [_P, _P, _I64, _P]),
     "tf_launch_count": (_I64, []),
+    "tf_launch_floor": (C.c_int, [_P]),
     "tf_rmsnorm": (C.c_int, [_P, _P, _P, _I32, _I32, C.c_float, _P]),
     "tf_silu_mul": (C.c_int, [_P, _P, _I32, _I32, _P]),
     "tf_kv_append": (C.c_int, [_I64, _P, _I32, _P, _P, _I32, _I32, _P, _P, _I64, _P]),

@@ -15,6 +15,8 @@
 //                   contiguous runs (a whole block of all layers is a single
 //                   2 MiB run in this layout) and submitted as ONE
 //                   cudaMemcpyBatchAsync; no SM is used at all.
+//   TF_ENGINE_CE2D - copy engines only: whole blocks as above, every partial
+//                   block as ONE 2-D copy (its runs are equally spaced).
 #include <algorithm>
 
 #include "tf_common.cuh"
@@ -194,6 +196,29 @@ static int swap_ce(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int
   return TF_OK;
 }
 
+// Copy-engine path for PARTIAL blocks: the n slots of one (block, layer, K|V,
+// head) run sit at the same offset in every run, and the runs of a block are
+// consecutive tiles of block_tokens * head_dim elements - so a partial block
+// over layers [l0, l1) is ONE 2-D copy (width n_slots * head_dim * 2 bytes,
+// height (l1 - l0) * 2 * kv_heads rows, pitch one tile) for the DMA engine,
+// instead of 2 * kv_heads * layers separate runs or an SM kernel.
+static int swap_ce2d(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int to_host,
+                     cudaStream_t st) {
+  const size_t pitch = (size_t)p.tile_elems * 2;
+  const size_t rows = (size_t)(l1 - l0) * 2 * p.kv_heads;
+  for (int32_t i = 0; i < n; ++i) {
+    const tf_seg& s = segs[i];
+    uint16_t* g = p.gpu + p.off(s.gpu_block, l0, 0, 0, s.slot_begin);
+    uint16_t* h = p.host + p.off(s.host_block, l0, 0, 0, s.slot_begin);
+    const size_t width = (size_t)s.n_slots * p.head_dim * 2;
+    if (to_host)
+      TF_CUDA(cudaMemcpy2DAsync(h, pitch, g, pitch, width, rows, cudaMemcpyDeviceToHost, st));
+    else
+      TF_CUDA(cudaMemcpy2DAsync(g, pitch, h, pitch, width, rows, cudaMemcpyHostToDevice, st));
+  }
+  return TF_OK;
+}
+
 static int swap_entry(int64_t pool, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int32_t engine,
                       int to_host, void* stream) {
   Pool* p = get_pool(pool);
@@ -212,9 +237,11 @@ static int swap_entry(int64_t pool, const tf_seg* segs, int32_t n, int32_t l0, i
   if (n == 0) return TF_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (engine == TF_ENGINE_CE) return swap_ce(*p, segs, n, l0, l1, to_host, st);
-  if (engine == TF_ENGINE_AUTO) {
-    // whole blocks (one contiguous run each) -> copy engines, no SMs;
-    // partial blocks (2*kv_heads*layers short runs each) -> one SM kernel
+  if (engine == TF_ENGINE_CE2D || engine == TF_ENGINE_AUTO) {
+    // whole blocks (all layers): one batched 1-D submission; every other
+    // segment: one 2-D copy each.  No SM is used at all (the copy engines
+    // beat the SM kernel at every chunk size, profiles/r2_wt_chunks_ce2d.json,
+    // and leave the SMs to the decode step).
     std::vector<tf_seg> full, part;
     const bool all_layers = (l0 == 0 && l1 == p->n_layers);
     for (int32_t i = 0; i < n; ++i)
@@ -223,8 +250,7 @@ static int swap_entry(int64_t pool, const tf_seg* segs, int32_t n, int32_t l0, i
       int rc = swap_ce(*p, full.data(), (int32_t)full.size(), l0, l1, to_host, st);
       if (rc != TF_OK) return rc;
     }
-    if (!part.empty()) return swap_sm(*p, part.data(), (int32_t)part.size(), l0, l1, to_host, st);
-    return TF_OK;
+    return part.empty() ? TF_OK : swap_ce2d(*p, part.data(), (int32_t)part.size(), l0, l1, to_host, st);
   }
   TF_CHECK_ARG(engine == TF_ENGINE_SM, "swap: unknown engine %d", engine);
   return swap_sm(*p, segs, n, l0, l1, to_host, st);

@@ -153,6 +153,7 @@ class GpuDataPlane:
         self.stats = {"d2h_tokens": 0, "h2d_tokens": 0, "d2h_launches": 0, "h2d_launches": 0, "append_tokens": 0,
                       "fill_tokens": 0, "attn_launches": 0, "decode_steps": 0}
         self._events = []  # (kind, tokens, start_evt, end_evt) for measured transfer rates
+        self._seglog = []  # per entry of _events: the chunk's (slot_begin, n_slots) segments (probe replays)
         ws = max(1, int(lib.tf_paged_decode_attn_workspace(pool.handle, max(1, len(reqs)), self.max_len, 64)))
         self._attn_ws = torch.zeros(ws, dtype=torch.uint8, device=dev)
         self.attn_out = None
@@ -394,6 +395,7 @@ class GpuDataPlane:
                                    self.swap_engine, C.c_void_p(st.cuda_stream)), "tf_kv_gather_d2h")
         t1.record(st)
         self._events.append(("d2h", ch.tokens, t0, t1))
+        self._seglog.append([(s0, n) for _, _, s0, n in segs])
         if ch.kind == "evict":
             f[lo:hi] = (f[lo:hi] & CLR_LIVE) | DETACHED
         self._d2h_busy = (rid, lo, hi, ch.kind, t1)
@@ -427,7 +429,7 @@ class GpuDataPlane:
         if self.mode == "realtime" and ev is not None:
             st.wait_event(ev)
         segs = self._segments(rid, miss)
-        if self.swap_engine != _lib.ENGINE_SM:
+        if self.swap_engine == _lib.ENGINE_CE:
             segs = self._widen_loads(rid, segs, miss)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -436,6 +438,7 @@ class GpuDataPlane:
                                     self.swap_engine, C.c_void_p(st.cuda_stream)), "tf_kv_scatter_h2d")
         t1.record(st)
         self._events.append(("h2d", ch.tokens, t0, t1))
+        self._seglog.append([(s0, n) for _, _, s0, n in segs])
         self.stats["h2d_tokens"] += ch.tokens
         self.stats["h2d_launches"] += 1
         # realtime: the request turns RUNNING only after the engine observed
@@ -443,11 +446,10 @@ class GpuDataPlane:
         return t0, t1
 
     def _widen_loads(self, rid, segs, miss):
-        """A partial-block load whose block holds nothing else (no other slot
-        LIVE / RESERVED / DETACHED) is issued as the whole block: one
-        contiguous run on the copy engines instead of 2*kv_heads*layers short
-        runs for the SM kernel, which would have to wait for SMs behind the
-        compute stream.  The extra slots carry host bytes no one reads (they
+        """(1-D copy-engine mode only) A partial-block load whose block holds
+        nothing else (no other slot LIVE / RESERVED / DETACHED) is issued as
+        the whole block: one contiguous run instead of 2*kv_heads*layers short
+        runs.  The default engine moves a partial block as one 2-D copy.  The extra slots carry host bytes no one reads (they
         lie beyond the request's context, or are refilled before use)."""
         f, tab = self.flags[rid], self.gtab[rid]
         loading = np.zeros(len(f), bool)

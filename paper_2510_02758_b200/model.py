@@ -320,19 +320,31 @@ class PagedDecoder:
                 self.pending[rid] = t
 
     @torch.no_grad()
-    def measure_attention(self, dp, rids, positions, reps=3):
+    def measure_attention(self, dp, rids, positions, reps=3, plan="exact"):
         """Time the paged-attention kernel on a live batch (all layers, CUDA
-        events on the launching stream) -> [(algorithmic bytes, ms)] per launch."""
+        events on the launching stream) -> [(algorithmic bytes, ms)] per launch.
+
+        plan="graph" launches it exactly as the captured decode graphs do: the
+        batch padded to its bucket with scratch rows (ctx 1) and max_ctx = the
+        pool's maximum context; plan="exact" uses B and max(ctx).  The
+        algorithmic bytes count the real rows only."""
         s = self.s
         st = dp.s_compute
         B = len(rids)
+        rows_l, pos_l = list(rids), list(positions)
+        max_ctx = max(positions) + 1
+        if plan == "graph" and self._graphs:
+            Bp = next(b for b in sorted(self._graphs) if b >= B)
+            rows_l += [dp.scratch_row] * (Bp - B)
+            pos_l += [0] * (Bp - B)
+            max_ctx = self._gmax_ctx
+        Bl = len(rows_l)
         with torch.cuda.stream(st):
-            rows = torch.tensor(rids, dtype=torch.int32, device=self.device)
-            ctx = torch.tensor([p + 1 for p in positions], dtype=torch.int32, device=self.device)
-            q = torch.randn((B, self.hq, s.head_dim), device=self.device).to(torch.bfloat16)
+            rows = torch.tensor(rows_l, dtype=torch.int32, device=self.device)
+            ctx = torch.tensor([p + 1 for p in pos_l], dtype=torch.int32, device=self.device)
+            q = torch.randn((Bl, self.hq, s.head_dim), device=self.device).to(torch.bfloat16)
             out = torch.empty_like(q)
-            max_ctx = max(positions) + 1
-            ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, B, max_ctx, self.hq)))
+            ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, Bl, max_ctx, self.hq)))
             ws = torch.zeros(ws_n, dtype=torch.uint8, device=self.device)
             abytes = (sum(positions) + B) * 2 * self.hkv * s.head_dim * 2 + 2 * B * self.hq * s.head_dim * 2 \
                 + sum((p + 16) // 16 for p in positions) * 4
@@ -343,7 +355,7 @@ class PagedDecoder:
                     e0.record(st)
                     check(lib.tf_paged_decode_attn(dp.pool.handle, C.c_void_p(q.data_ptr()),
                                                    C.c_void_p(dp.table.data_ptr()), dp.nlb,
-                                                   C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), B,
+                                                   C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), Bl,
                                                    max_ctx, li, self.hq, self.scale, C.c_void_p(out.data_ptr()),
                                                    C.c_void_p(ws.data_ptr()), ws_n, C.c_void_p(st.cuda_stream)),
                           "tf_paged_decode_attn")

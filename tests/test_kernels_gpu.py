@@ -34,7 +34,7 @@ def _segs(lib, segs):
     return arr
 
 
-@pytest.mark.parametrize("engine", [0, 1, 2])
+@pytest.mark.parametrize("engine", [0, 1, 2, 3])
 @pytest.mark.parametrize("shape", [(2, 2, 64), (32, 8, 128)])
 def test_swap_roundtrip(cuda, engine, shape):
     L, H, D = shape
