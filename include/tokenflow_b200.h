@@ -49,7 +49,7 @@ extern "C" {
 #define TF_TIER_GPU 0
 #define TF_TIER_HOST 1
 #define TF_ENGINE_SM 0 /* SM-driven zero-copy gather/scatter kernel */
-#define TF_ENGINE_CE 1 /* copy engines (cudaMemcpyBatchAsync of contiguous runs) */
+#define TF_ENGINE_CE 1 /* copy engines (one cudaMemcpyAsync per maximal contiguous run) */
 #define TF_ENGINE_AUTO 2 /* = TF_ENGINE_CE2D (kept for callers of ABI v1) */
 #define TF_ENGINE_CE2D 3 /* copy engines only: whole blocks batched, each partial block one 2-D copy */
 

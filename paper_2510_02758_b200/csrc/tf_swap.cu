@@ -13,8 +13,8 @@
 //                   decode step keeps the rest of the machine.
 //   TF_ENGINE_CE  - copy engines: the segments are coalesced into maximal
 //                   contiguous runs (a whole block of all layers is a single
-//                   2 MiB run in this layout) and submitted as ONE
-//                   cudaMemcpyBatchAsync; no SM is used at all.
+//                   2 MiB run in this layout, LIFO-adjacent blocks merge into
+//                   longer ones), one cudaMemcpyAsync per run; no SM is used.
 //   TF_ENGINE_CE2D - copy engines only: whole blocks as above, every partial
 //                   block as ONE 2-D copy (its runs are equally spaced).
 #include <algorithm>
@@ -143,7 +143,7 @@ static int swap_sm(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int
   return TF_OK;
 }
 
-// Copy-engine path: maximal contiguous runs, one batched submission.
+// Copy-engine path: maximal contiguous runs, one submission per run.
 static int swap_ce(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int to_host,
                    cudaStream_t st) {
   std::vector<void*> dst, src;
@@ -178,21 +178,10 @@ static int swap_ce(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int
           push(p.off(s.gpu_block, l, kv, h, s.slot_begin), p.off(s.host_block, l, kv, h, s.slot_begin),
                (int64_t)s.n_slots * p.head_dim);
   }
-  if (sz.empty()) return TF_OK;
-  cudaMemcpyAttributes attr;
-  memset(&attr, 0, sizeof(attr));
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  attr.srcLocHint.type = to_host ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
-  attr.dstLocHint.type = to_host ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
-  size_t attr_idx = 0, fail = 0;
-  cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), sz.size(), &attr, &attr_idx, 1, &fail, st);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    // Fall back to individual async copies (same engines, more submissions).
-    for (size_t i = 0; i < sz.size(); ++i)
-      TF_CUDA(cudaMemcpyAsync(dst[i], src[i], sz[i], to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st));
-  }
+  // One plain async copy per maximal run: few, large submissions (a chunk of
+  // whole blocks is typically a handful of multi-MiB runs).
+  for (size_t i = 0; i < sz.size(); ++i)
+    TF_CUDA(cudaMemcpyAsync(dst[i], src[i], sz[i], to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st));
   return TF_OK;
 }
 
@@ -238,7 +227,7 @@ static int swap_entry(int64_t pool, const tf_seg* segs, int32_t n, int32_t l0, i
   cudaStream_t st = (cudaStream_t)stream;
   if (engine == TF_ENGINE_CE) return swap_ce(*p, segs, n, l0, l1, to_host, st);
   if (engine == TF_ENGINE_CE2D || engine == TF_ENGINE_AUTO) {
-    // whole blocks (all layers): one batched 1-D submission; every other
+    // whole blocks (all layers): merged 1-D runs; every other
     // segment: one 2-D copy each.  No SM is used at all (the copy engines
     // beat the SM kernel at every chunk size, profiles/r2_wt_chunks_ce2d.json,
     // and leave the SMs to the decode step).
