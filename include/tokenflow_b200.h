@@ -346,6 +346,40 @@ int tf_select_batch(int64_t sel, const tf_prio* views, int32_t n, double gpu_mem
 /* glibc-exact exp, exported for the oracle checks */
 double tf_host_glibc_exp(double x);
 
+
+/* ---- C4 tensor-parallel data path: peer-memory all-reduce
+ * fused with the residual add and the next RMSNorm.  Replaces the NCCL
+ * all-reduce after o_proj / down_proj of the TP decoder (the reference has
+ * no TP: tokensim/engine.py:1089-1091 runs one replica per GPU; C4 is the
+ * north-star configuration built on top of it).
+ *
+ * tf_ar_create   this rank's communicator on the current device: a cudaMalloc'ed
+ *                data buffer of capacity_bytes (the rank's GEMM partial goes
+ *                there: tf_ar_buffer) + a zeroed control block (barrier flags).
+ * tf_ar_export   128 bytes: IPC handles of the data buffer and control block.
+ * tf_ar_open     all_handles = world x 128 bytes in rank order: maps every
+ *                peer's buffer and control block (cudaIpcOpenMemHandle; P2P
+ *                over NVLink between GPUs, plain aliases on one device).
+ * tf_ar_set_peers  same-process ranks (tests): peers' device pointers directly.
+ * tf_ar_residual_rmsnorm
+ *                x[r] = bf16(x[r] + sum_p part_p[r]) (fp32, rank order: bit-identical
+ *                on every rank); h_out[r] = rmsnorm(x[r]) * gamma.  x NULL: the
+ *                plain sum (to h_out when gamma is NULL).  rows x dim bf16,
+ *                dim % 8 == 0, dim <= 8192.  Every rank must issue the same
+ *                sequence of calls with the same rows; graph-capturable.
+ * tf_ar_status   1 if a barrier wait timed out (10 s) since creation, else 0 (syncs).
+ */
+int tf_ar_create(int32_t rank, int32_t world, int64_t capacity_bytes, int64_t* out_handle);
+void* tf_ar_buffer(int64_t ar);
+void* tf_ar_ctl(int64_t ar);
+int tf_ar_export(int64_t ar, void* out128);
+int tf_ar_open(int64_t ar, const void* all_handles);
+int tf_ar_set_peers(int64_t ar, void* const* data, void* const* ctl);
+int tf_ar_residual_rmsnorm(int64_t ar, void* x, const void* gamma, void* h_out, int32_t rows, int32_t dim, float eps,
+                           void* stream);
+int tf_ar_status(int64_t ar);
+int tf_ar_destroy(int64_t ar);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,7 @@ UNITS = {
     "tf_attn_tma.cu": [],
     "tf_ops.cu": [],
     "tf_select.cu": ["-fmad=false"],
+    "tf_ar.cu": [],
 }
 
 
@@ -46,14 +47,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return OUT
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
-    objs = []
+    cmds, objs = [], []
     for unit, extra in UNITS.items():
         obj = objdir / (unit + ".o")
-        cmd = [NVCC, *COMMON, *extra, "-c", str(CSRC / unit), "-o", str(obj)]
+        cmds.append([NVCC, *COMMON, *extra, "-c", str(CSRC / unit), "-o", str(obj)])
+        objs.append(str(obj))
+    # translation units are independent: compile them in parallel
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(cmd):
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
-        objs.append(str(obj))
+
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        list(ex.map(run, cmds))
     tmp = OUT.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
     if verbose:

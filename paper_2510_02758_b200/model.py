@@ -102,6 +102,7 @@ class PagedDecoder:
         self._inv_freq = inv
         self.pending = {}  # rid -> next token to emit
         self.history = {}  # rid -> generated tokens (for recompute)
+        self.keep_logits, self.last_logits = False, None
         self.prompts = {}
         self._unresolved = {}  # rid -> (pinned buffer, column) of an in-flight prefill's t0/t1
         self.scale = 1.0 / math.sqrt(hd)
@@ -138,6 +139,14 @@ class PagedDecoder:
                              C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tf_rmsnorm")
         return y
 
+    def _sample_normed(self, h):
+        """Greedy next token from the final-normed hidden states; with
+        ``keep_logits`` set (tests, eager only) the logits stay in ``last_logits``."""
+        lg = h @ self.lm_head
+        if self.keep_logits:
+            self.last_logits = lg
+        return lg.argmax(-1)
+
     def _rope(self, x, pos):
         # x [n, heads, hd], pos [n] (int64)
         ang = pos.float()[:, None] * self._inv_freq[None, :]
@@ -165,13 +174,32 @@ class PagedDecoder:
     def _qkv(self, h, L):
         return torch.addmm(L["bqkv"], h, L["wqkv"]) if "bqkv" in L else h @ L["wqkv"]
 
-    def _mlp(self, x, L):
-        h = self._rms(x, L["ln2"])
+    def _proj_residual_norm(self, x, a, w, gamma):
+        """(x + a @ w, rmsnorm(x + a @ w) * gamma): a sub-layer's output
+        projection, its residual and the next sub-layer's input norm.  Under
+        TP with a peer-memory communicator (tp.PeerAllReduce) the rank's GEMM
+        writes its partial into its registered buffer and ONE kernel
+        (tf_ar_residual_rmsnorm) does the all-reduce over NVLink, the residual
+        add and the norm; otherwise addmm (+ NCCL all-reduce) and tf_rmsnorm."""
+        ar = getattr(self.tp, "ar", None) if self.tp is not None and self.tp.size > 1 else None
+        if ar is None or not ar.fits(x.shape[0], x.shape[1]):
+            x = self._proj_residual(x, a, w)
+            return x, self._rms(x, gamma)
+        part = ar.partial(x.shape[0], x.shape[1])
+        torch.mm(a, w, out=part)
+        h = torch.empty_like(x)
+        ar.residual_rmsnorm(x, gamma, h, self.s.rms_eps, torch.cuda.current_stream())
+        return x, h
+
+    def _mlp_act(self, h, L):
         gu = h @ L["wgu"]
         act = torch.empty((gu.shape[0], self.ffn), device=gu.device, dtype=gu.dtype)
         check(lib.tf_silu_mul(C.c_void_p(gu.data_ptr()), C.c_void_p(act.data_ptr()), gu.shape[0], self.ffn,
                               C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tf_silu_mul")
-        return self._proj_residual(x, act, L["wd"])
+        return act
+
+    def _next_norm(self, li):
+        return self.layers[li + 1]["ln1"] if li + 1 < len(self.layers) else self.ln_f
 
     # ------------------------------------------------------------ forward passes
     @torch.no_grad()
@@ -206,8 +234,8 @@ class PagedDecoder:
         q = torch.empty((n, self.hq, s.head_dim), device=self.device, dtype=x.dtype)
         kvb = torch.empty((2, n, self.hkv, s.head_dim), device=self.device, dtype=x.dtype)
         k, v = kvb[0], kvb[1]
+        h = self._rms(x, self.layers[0]["ln1"])
         for li, L in enumerate(self.layers):
-            h = self._rms(x, L["ln1"])
             qkv = self._qkv(h, L)
             # rotary q/k + paged K/V append (+ host mirror when write-through is
             # fused) + contiguous k/v for the prompt attention
@@ -231,9 +259,9 @@ class PagedDecoder:
             kx = k.repeat_interleave(G, dim=1) if G > 1 else k
             vx = v.repeat_interleave(G, dim=1) if G > 1 else v
             a = varlen_attn(q, kx, vx, cu, cu, max_len, max_len, window_size=(-1, 0)).reshape(n, -1)
-            x = self._proj_residual(x, a, L["wo"])
-            x = self._mlp(x, L)
-        return (self._rms(x[last], self.ln_f) @ self.lm_head).argmax(-1)
+            x, h = self._proj_residual_norm(x, a, L["wo"], L["ln2"])
+            x, h = self._proj_residual_norm(x, self._mlp_act(h, L), L["wd"], self._next_norm(li))
+        return self._sample_normed(h[last])
 
     @torch.no_grad()
     def prefill(self, dp, job, spans, eng):
@@ -505,8 +533,8 @@ class PagedDecoder:
             abytes = (sum(positions) + B) * 2 * self.hkv * s.head_dim * 2 + 2 * B * self.hq * s.head_dim * 2 \
                 + sum((p + 16) // 16 for p in positions) * 4
         q = torch.empty((B, self.hq, s.head_dim), device=self.device, dtype=x.dtype)
+        h = self._rms(x, self.layers[0]["ln1"])
         for li, L in enumerate(self.layers):
-            h = self._rms(x, L["ln1"])
             qkv = self._qkv(h, L)
             # fused rotary embedding + paged K/V append + q layout (one launch)
             if getattr(dp, "fused_wt", False):
@@ -534,6 +562,6 @@ class PagedDecoder:
             if timing is not None:
                 e1.record(st)
                 timing.append((abytes, e0, e1))
-            x = self._proj_residual(x, attn.view(B, -1), L["wo"])
-            x = self._mlp(x, L)
-        return (self._rms(x, self.ln_f) @ self.lm_head).argmax(-1)
+            x, h = self._proj_residual_norm(x, attn.view(B, -1), L["wo"], L["ln2"])
+            x, h = self._proj_residual_norm(x, self._mlp_act(h, L), L["wd"], self._next_norm(li))
+        return self._sample_normed(h)

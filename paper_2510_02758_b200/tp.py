@@ -7,9 +7,13 @@ over its OWN host link - so swap bytes per rank are bytes/TP, in lockstep.
 
 Two collectives, nothing else:
 
-* data path: one NCCL all-reduce (sum) after o_proj and one after down_proj
-  per layer (B x hidden bf16 each), on the compute stream
-  (``model.PagedDecoder`` with ``tp=TpGroup(...)``);
+* data path: one all-reduce (sum) after o_proj and one after down_proj per
+  layer (B x hidden bf16 each), on the compute stream (``model.PagedDecoder``
+  with ``tp=TpGroup(...)``).  With a ``PeerAllReduce`` attached (the default
+  of ``bench.py --config c4``) each rank's GEMM writes its partial into a
+  registered buffer and one kernel (``tf_ar_residual_rmsnorm``) reads the
+  peers' partials over NVLink, adds the residual and applies the next RMSNorm
+  - graph-capturable, no NCCL on the data path; without it, NCCL;
 * control path: ``Lockstep.agree`` - one 10-double all-reduce (max) per loop
   iteration of the real-time engine over a CPU (gloo) group.  Instead of
   broadcasting rank 0's decisions, every rank runs the same deterministic
@@ -72,8 +76,9 @@ class TpGroup:
     """This rank's slice of a TP model: rank, size and the NCCL group of the
     data-path all-reduces."""
 
-    def __init__(self, rank: int, size: int, group=None):
+    def __init__(self, rank: int, size: int, group=None, ar: "PeerAllReduce | None" = None):
         self.rank, self.size, self.group = rank, size, group
+        self.ar = ar  # peer-memory data path (None: NCCL all-reduce)
 
     def heads(self, n: int) -> range:
         if n % self.size:
@@ -91,3 +96,79 @@ class TpGroup:
         if self.size > 1:
             dist.all_reduce(x, group=self.group)
         return x
+
+
+class PeerAllReduce:
+    """This rank's peer-memory all-reduce communicator (csrc/tf_ar.cu).
+
+    Buffers are cudaMalloc'ed by the library and mapped into every peer with
+    CUDA IPC handles exchanged once over ``group`` (any torch.distributed
+    backend; gloo works).  Ranks living in one process (tests) are linked
+    with ``PeerAllReduce.link`` instead."""
+
+    def __init__(self, rank: int, world: int, capacity_bytes: int, device=None):
+        from . import _lib
+
+        self._lib = _lib
+        self.rank, self.world, self.capacity = rank, world, int(capacity_bytes)
+        h = _lib.C.c_int64()
+        _lib.check(_lib.lib.tf_ar_create(rank, world, self.capacity, _lib.C.byref(h)), "tf_ar_create")
+        self.handle = h.value
+        ptr = _lib.lib.tf_ar_buffer(self.handle)
+
+        class _Cai:  # zero-copy torch view of the library-owned buffer
+            __cuda_array_interface__ = {"shape": (self.capacity // 2,), "typestr": "<i2", "data": (ptr, False),
+                                        "version": 2}
+
+        self._buf = torch.as_tensor(_Cai(), device=device or torch.device("cuda", torch.cuda.current_device()))
+        self._buf = self._buf.view(torch.bfloat16)
+
+    @classmethod
+    def from_group(cls, rank: int, world: int, capacity_bytes: int, group=None, device=None) -> "PeerAllReduce":
+        self = cls(rank, world, capacity_bytes, device)
+        C = self._lib.C
+        mine = (C.c_uint8 * 128)()
+        self._lib.check(self._lib.lib.tf_ar_export(self.handle, mine), "tf_ar_export")
+        every = [None] * world
+        dist.all_gather_object(every, bytes(mine), group=group)
+        allh = (C.c_uint8 * (128 * world)).from_buffer_copy(b"".join(every))
+        self._lib.check(self._lib.lib.tf_ar_open(self.handle, allh), "tf_ar_open")
+        return self
+
+    @staticmethod
+    def link(ranks) -> None:
+        """Same-process ranks (one per thread / stream): every rank sees the
+        others' buffers directly."""
+        from . import _lib
+
+        n = len(ranks)
+        data = (_lib.C.c_void_p * n)(*[_lib.lib.tf_ar_buffer(r.handle) for r in ranks])
+        ctl = (_lib.C.c_void_p * n)(*[_lib.lib.tf_ar_ctl(r.handle) for r in ranks])
+        for r in ranks:
+            _lib.check(_lib.lib.tf_ar_set_peers(r.handle, data, ctl), "tf_ar_set_peers")
+
+    def fits(self, rows: int, dim: int) -> bool:
+        return rows * dim * 2 <= self.capacity
+
+    def partial(self, rows: int, dim: int) -> torch.Tensor:
+        """[rows, dim] bf16 view of this rank's registered buffer (GEMM output)."""
+        return self._buf[: rows * dim].view(rows, dim)
+
+    def residual_rmsnorm(self, x, gamma, h_out, eps, stream=None) -> None:
+        """x += sum over ranks of partial(x.shape); h_out = rmsnorm(x) * gamma."""
+        C = self._lib.C
+        rows, dim = x.shape
+        st = stream if stream is not None else torch.cuda.current_stream()
+        self._lib.check(self._lib.lib.tf_ar_residual_rmsnorm(
+            self.handle, C.c_void_p(x.data_ptr()), C.c_void_p(gamma.data_ptr()) if gamma is not None else None,
+            C.c_void_p(h_out.data_ptr()) if h_out is not None else None, rows, dim, eps,
+            C.c_void_p(st.cuda_stream)), "tf_ar_residual_rmsnorm")
+
+    def status(self) -> int:
+        return int(self._lib.lib.tf_ar_status(self.handle))
+
+    def close(self) -> None:
+        if self.handle:
+            self._buf = None
+            self._lib.lib.tf_ar_destroy(self.handle)
+            self.handle = 0

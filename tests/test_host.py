@@ -150,7 +150,7 @@ def test_library_exports_every_header_symbol():
     from paper_2510_02758_b200 import _lib
 
     hdr = (ROOT / "include" / "tokenflow_b200.h").read_text()
-    declared = set(re.findall(r"^\s*(?:const char\*|int64_t|int|double)\s+(tf_\w+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:const char\*|void\*|int64_t|int|double)\s+(tf_\w+)\s*\(", hdr, re.M))
     assert declared, "no declarations parsed"
     assert declared == set(_lib.SIGNATURES)
     for name in declared:

@@ -105,3 +105,75 @@ def test_graph_decode_matches_eager(cuda):
     a = kv_graph.view(64, -1)[blocks].view(torch.bfloat16).float()
     b = pool.gpu.view(64, -1)[blocks].view(torch.bfloat16).float()
     assert torch.allclose(a, b, atol=3e-2, rtol=3e-2)
+
+
+def _host_mirror_mismatches(dp, eng, fused):
+    """Byte check of the host tier against HBM: every position the engine
+    counts as mirrored on the host (fused: HOSTV flags set by the decode /
+    prefill epilogue; reference write-through: the prefix [0, cpu_synced) of
+    landed chunks, tokensim/kvstore.py:112-141) that is still LIVE in HBM must
+    hold the same bf16 bits in both tiers, for every layer / K|V / head."""
+    import numpy as np
+    import torch
+
+    from paper_2510_02758_b200.dataplane import HOSTV, LIVE
+
+    torch.cuda.synchronize()
+    gv, hv = dp.pool.gpu_view(), dp.pool.host_view()
+    checked = bad = 0
+    for rid, s in eng.state.items():
+        if s.status in ("gen_done", "done"):
+            continue
+        f = dp.flags[rid]
+        m = (f & LIVE) != 0
+        if fused:
+            m &= (f & HOSTV) != 0
+        else:
+            m[s.kv.cpu_synced:] = False
+        pos = np.nonzero(m)[0]
+        if not len(pos):
+            continue
+        j, slot = pos // dp.B, pos % dp.B
+        g = torch.from_numpy(dp.gtab[rid][j].astype(np.int64))
+        h = torch.from_numpy(dp.htab[rid][j].astype(np.int64))
+        assert (g >= 0).all() and (h >= 0).all()
+        sl = torch.from_numpy(slot.astype(np.int64))
+        a = gv[g.to(gv.device), :, :, :, sl.to(gv.device)].cpu()
+        b = hv[h, :, :, :, sl]
+        checked += len(pos)
+        bad += int((a != b).reshape(len(pos), -1).any(dim=1).sum())
+    return checked, bad
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_host_tier_bytes_equal_hbm_during_serving(cuda, fused, monkeypatch):
+    """Fused write-through (tf_rope_kv_append_wt) and the reference's chunked
+    write-through must leave byte-identical host copies of every mirrored
+    position; checked every 20 decode steps of a C1 real-time run."""
+    from paper_2510_02758_b200 import dataplane as dpmod
+
+    seen = {"checked": 0, "bad": 0, "calls": 0}
+    orig = dpmod.GpuDataPlane.decode_done
+    state = {}
+
+    def decode_done(self, batch, made):
+        orig(self, batch, made)
+        seen["calls"] += 1
+        if seen["calls"] % 20 == 0 and "eng" in state:
+            c, b = _host_mirror_mismatches(self, state["eng"], fused)
+            seen["checked"] += c
+            seen["bad"] += b
+
+    from paper_2510_02758_b200.realtime import RealtimeEngine
+
+    orig_init = RealtimeEngine.__init__
+
+    def init(self, *a, **k):
+        orig_init(self, *a, **k)
+        state["eng"] = self
+
+    monkeypatch.setattr(dpmod.GpuDataPlane, "decode_done", decode_done)
+    monkeypatch.setattr(RealtimeEngine, "__init__", init)
+    _run(cuda, engine=2, graphs=True, fused=fused)
+    assert seen["checked"] > 1000, seen
+    assert seen["bad"] == 0, seen
