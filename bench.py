@@ -181,12 +181,21 @@ def run_ours(args):
             import torch.distributed as dist
 
             lockstep = Lockstep(dist.new_group(backend="gloo"))
+            if args.tp_data == "peer":
+                # data path: each rank's o_proj / down_proj partial goes into its
+                # registered buffer, one kernel reads the peers' over NVLink and
+                # fuses residual + RMSNorm (csrc/tf_ar.cu); handles over gloo
+                from paper_2510_02758_b200.tp import PeerAllReduce
+
+                tp.ar = PeerAllReduce.from_group(rank, world, 8192 * configs.c4(world).model.hidden * 2,
+                                                 group=lockstep.group, device=dev)
         c2 = configs.c4(world)
         tr = _trace_for_rank(0, 1, args.arrivals)
         if world > 1 and args.graphs and one_gpu:
-            # the one-GPU dry run carries the all-reduces over gloo, which cannot
-            # be captured; over NCCL (the real C4 run) the decode forward WITH its
-            # all-reduces is captured per bucket like the TP=1 one
+            # the one-GPU dry run shares one device between the ranks' processes
+            # (time-sliced contexts): run it eager.  On a real C4 run the decode
+            # forward WITH its all-reduces (peer kernel or NCCL) is captured per
+            # bucket like the TP=1 one
             args.graphs = 0
     else:
         c2 = configs.C2
@@ -875,6 +884,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c2", "c4"], help="c2: Llama3-8B replicas (C2/C3, default); "
                     "c4: Qwen2.5-32B tensor-parallel over the launched ranks")
     ap.add_argument("--graphs", type=int, default=1)
+    ap.add_argument("--tp-data", default="peer", choices=["peer", "nccl"],
+                    help="c4 data path: peer-memory all-reduce fused with residual + RMSNorm (default) or NCCL")
     ap.add_argument("--fused-wt", type=int, default=0, help="1: mirror KV to the host inside the prefill/decode "
                     "epilogue (SURVEY 8f #1) instead of the reference's write-through chunks.  Off by default: it "
                     "makes every preemption an instant full release, which tips the reference policy into "

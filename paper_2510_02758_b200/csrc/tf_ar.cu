@@ -143,9 +143,17 @@ __global__ void __launch_bounds__(kArThreads) ar_residual_rmsnorm_kernel(const _
   }
   __syncthreads();
   const uint32_t e = s_epoch;
+  const int nv = a.dim / 8;
+  // the norm weights (local, not written by peers): loaded once per CTA, while
+  // the start barrier waits
+  uint4 gw[kArMaxVec];
+#pragma unroll
+  for (int k = 0; k < kArMaxVec; ++k) {
+    const int i = threadIdx.x + k * kArThreads;
+    gw[k] = (a.gamma && i < nv) ? __ldg(reinterpret_cast<const uint4*>(a.gamma) + i) : make_uint4(0, 0, 0, 0);
+  }
   ar_barrier(a, 0, e);
 
-  const int nv = a.dim / 8;
   for (int r = blockIdx.x; r < a.rows; r += gridDim.x) {
     const int64_t base = (int64_t)r * a.dim;
     float v[kArMaxVec][8];
@@ -194,7 +202,7 @@ __global__ void __launch_bounds__(kArThreads) ar_residual_rmsnorm_kernel(const _
         const int i = threadIdx.x + k * kArThreads;
         if (i < nv) {
           float g[8], o[8];
-          unpack8f(__ldg(reinterpret_cast<const uint4*>(a.gamma) + i), g);
+          unpack8f(gw[k], g);
 #pragma unroll
           for (int j = 0; j < 8; ++j) o[j] = __bfloat162float(__float2bfloat16_rn(v[k][j] * rs)) * g[j];
           reinterpret_cast<uint4*>(a.h_out + base)[i] = pack8f(o);

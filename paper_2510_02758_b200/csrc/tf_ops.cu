@@ -42,7 +42,15 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* _
   uint4* yr = reinterpret_cast<uint4*>(y + row * D);
   const int nv = D / 8;
   float v[kNormMaxVec][8];
+  uint4 gw[kNormMaxVec];
   float ss = 0.f;
+  // the weight loads are issued with the row's (independent of the reduction)
+  // so their latency overlaps instead of following it
+#pragma unroll
+  for (int k = 0; k < kNormMaxVec; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < nv) gw[k] = __ldg(wr + i);
+  }
 #pragma unroll
   for (int k = 0; k < kNormMaxVec; ++k) {
     const int i = threadIdx.x + k * kNormThreads;
@@ -66,7 +74,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* _
     const int i = threadIdx.x + k * kNormThreads;
     if (i < nv) {
       float g[8], o[8];
-      unpack8(__ldg(wr + i), g);
+      unpack8(gw[k], g);
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(v[k][e] * r)) * g[e];
       yr[i] = pack8(o);

@@ -90,6 +90,8 @@ def main():
     ap.add_argument("--impls", default="0,3,5", help="comma list of implementations (tf_paged_decode_attn_impl)")
     ap.add_argument("--layout", default="random", choices=["random", "contig"])
     ap.add_argument("--pool-blocks", type=int, default=22000)
+    ap.add_argument("--orders", default="asis", help="comma list: asis (random order), desc (longest context "
+                    "first = LPT order of the CTAs)")
     args = ap.parse_args()
     global LAYOUT
     LAYOUT = args.layout
@@ -108,14 +110,17 @@ def main():
                 if args.only and args.only != f"{B}:{name}:{plan}":
                     continue
                 plan_ctx = max(ctxs) if plan == "exact" else 4096
-                for impl in [int(x) for x in args.impls.split(",")]:
-                    _lib.lib.tf_paged_decode_attn_impl(impl)
-                    ms, ab = run_case(pool, B, [int(c) for c in ctxs], plan_ctx, reps=args.reps)
-                    gbs = ab / (ms / 1e3) / 1e9
-                    row = {"impl": impl, "B": B, "ctx": name, "plan": plan, "us": round(ms * 1e3, 2),
-                           "MB": round(ab / 1e6, 1), "gbs": round(gbs, 1), "frac": round(gbs / pk, 4)}
-                    cases.append(row)
-                    print(json.dumps(row), flush=True)
+                for order in args.orders.split(","):
+                    cc = sorted(ctxs, reverse=True) if order == "desc" else ctxs
+                    for impl in [int(x) for x in args.impls.split(",")]:
+                        _lib.lib.tf_paged_decode_attn_impl(impl)
+                        ms, ab = run_case(pool, B, [int(c) for c in cc], plan_ctx, reps=args.reps)
+                        gbs = ab / (ms / 1e3) / 1e9
+                        row = {"impl": impl, "B": B, "ctx": name, "plan": plan, "order": order,
+                               "us": round(ms * 1e3, 2), "MB": round(ab / 1e6, 1), "gbs": round(gbs, 1),
+                               "frac": round(gbs / pk, 4)}
+                        cases.append(row)
+                        print(json.dumps(row), flush=True)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps({"peak_gbs": pk, "cases": cases}, indent=1))
 
