@@ -102,7 +102,7 @@ class PagedDecoder:
         self._inv_freq = inv
         self.pending = {}  # rid -> next token to emit
         self.history = {}  # rid -> generated tokens (for recompute)
-        self.keep_logits, self.last_logits = False, None
+        self.keep_logits, self.last_logits, self.graph_logits = False, None, {}
         self.prompts = {}
         self._unresolved = {}  # rid -> (pinned buffer, column) of an in-flight prefill's t0/t1
         self.scale = 1.0 / math.sqrt(hd)
@@ -424,6 +424,8 @@ class PagedDecoder:
                 out = self._forward_graphable(dp, io, Bp, ws, torch.cuda.current_stream())
             self._graph_launches[("decode", Bp)] = lib.tf_launch_count() - c0
             self._graphs[Bp] = (g, io, stage, out, ws)
+            if self.keep_logits:  # the bucket's static logits (tests)
+                self.graph_logits[Bp] = self.last_logits
         st.synchronize()
         if prefill_buckets:
             self._capture_recompute_graphs(dp, mempool, st, prefill_buckets)

@@ -83,7 +83,9 @@ def test_graph_decode_matches_eager(cuda):
     tab = torch.tensor(free[:20], dtype=torch.int32, device=cuda).view(5, 4)
     dp.table[:5, :4] = tab
     pool.gpu.copy_((torch.randn(pool.gpu.numel(), device=cuda) * 0.3).to(torch.bfloat16).view(torch.int16))
+    model.keep_logits = True  # the captured bucket's static logits tensor -> graph_logits[8]
     model.enable_graphs(dp, buckets=(8,))
+    g_logits = model.graph_logits[8]
     rids, pos = [0, 2, 3], [40, 54, 61]
     for r in rids:
         model.pending[r] = 100 + r
@@ -98,9 +100,18 @@ def test_graph_decode_matches_eager(cuda):
         toks = torch.tensor([100 + r for r in rids], device=cuda)
         e_out = model._decode_rows(dp, rids, toks, pos, st)
     st.synchronize()
-    # the graph plans attention splits for the pool's maximum context, the eager
-    # path for this batch's: same math, different fp32 summation order
-    assert (g_out == e_out).float().mean().item() >= 2 / 3
+    # the graph plans attention for the pool's maximum context (and pads the
+    # batch to its bucket), the eager path for this batch's: same math,
+    # different fp32 summation order -> logits within 2e-2 of max |logit|,
+    # and the same greedy token wherever the top-2 margin exceeds that
+    lg = g_logits[: len(rids)].float()
+    le = model.last_logits.float()
+    err = (lg - le).abs().amax(-1)
+    tol = 2e-2 * le.abs().amax(-1) + 2.0 ** -8
+    assert bool((err <= tol).all()), (err.tolist(), tol.tolist())
+    top2 = le.topk(2, dim=-1).values
+    clear = (top2[:, 0] - top2[:, 1]) > 2 * tol
+    assert torch.equal(g_out[clear], e_out[clear])
     blocks = tab[rids].flatten().long()
     a = kv_graph.view(64, -1)[blocks].view(torch.bfloat16).float()
     b = pool.gpu.view(64, -1)[blocks].view(torch.bfloat16).float()
