@@ -7,7 +7,7 @@ heads x 128 x bf16).  For block counts 1, 2, 4, ..., max: a random
 permutation of pool block ids (seed 0) is gathered to (d2h) / scattered from
 (h2d) pinned host blocks, either all 32 layers per launch or one layer per
 launch (per-layer chunking), with the SM zero-copy kernel (engine 0) and the
-copy-engine batch path (engine 1); plus both directions concurrently on two
+copy-engine path (engine 1: one cudaMemcpyAsync per maximal contiguous run; engine 3: + one 2-D copy per partial block); plus both directions concurrently on two
 streams.  GB/s are reported against PCIe Gen5 x16 (63.0 GB/s per direction)
 and against the box's measured contiguous pinned cudaMemcpyAsync peak.
 
@@ -114,7 +114,7 @@ def sweep(args):
                 tb = max(e0.elapsed_time(e1), e0.elapsed_time(e2)) / 1e3 / reps
                 del t0
                 nbytes = n * bb
-                rows.append({"blocks": n, "engine": "sm" if eng == 0 else "ce", "per_layer": per_layer,
+                rows.append({"blocks": n, "engine": {0: "sm", 1: "ce", 2: "auto", 3: "ce2d"}[eng], "per_layer": per_layer,
                              "bytes": nbytes, "d2h_gbs": nbytes / td / 1e9, "h2d_gbs": nbytes / th / 1e9,
                              "duplex_gbs": 2 * nbytes / tb / 1e9,
                              "d2h_frac_pcie": nbytes / td / 1e9 / PCIE, "h2d_frac_pcie": nbytes / th / 1e9 / PCIE,
@@ -233,7 +233,7 @@ def overlap(pool, args):
         t_swp = run([swaps])
         t_both = run([decode, swaps])
         hidden = 1.0 - max(0.0, t_both - t_dec) / t_swp
-        res["sm" if eng == 0 else "ce"] = {"t_decode_ms": t_dec * 1e3, "t_swap_ms": t_swp * 1e3,
+        res[{0: "sm", 1: "ce", 2: "auto", 3: "ce2d"}[eng]] = {"t_decode_ms": t_dec * 1e3, "t_swap_ms": t_swp * 1e3,
                                            "t_both_ms": t_both * 1e3, "hidden_frac": hidden,
                                            "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = 32 layers of "
                                                    "paged attention B=64 ctx=2600; swap = NB x 2 MiB out + NB x 2 MiB in, concurrent"}

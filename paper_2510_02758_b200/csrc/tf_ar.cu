@@ -99,6 +99,9 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 // handle one peer).  Returns after every rank reached the same phase of call e.
 __device__ __forceinline__ void ar_barrier(const ArArgs& a, int phase, uint32_t e) {
   const int c = blockIdx.x;
+  // every thread's earlier accesses (phase 1: its reads of the peers' buffers)
+  // happen before the release below
+  __syncthreads();
   if (threadIdx.x < (unsigned)a.world) {
     const int p = threadIdx.x;
     __threadfence_system();

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 
 import torch
@@ -103,6 +104,7 @@ class PagedDecoder:
         self.pending = {}  # rid -> next token to emit
         self.history = {}  # rid -> generated tokens (for recompute)
         self.keep_logits, self.last_logits, self.graph_logits = False, None, {}
+        self.lpt_order = os.environ.get("TF_LPT", "0") == "1"  # decode rows longest-context first
         self.prompts = {}
         self._unresolved = {}  # rid -> (pinned buffer, column) of an in-flight prefill's t0/t1
         self.scale = 1.0 / math.sqrt(hd)
@@ -321,6 +323,11 @@ class PagedDecoder:
     @torch.no_grad()
     def decode(self, dp, batch, eng):
         st = dp.s_compute
+        if self.lpt_order:
+            # longest context first: attention CTAs are dispatched in row order,
+            # so the long (request, head) items start in the first wave and the
+            # tail wave holds the short ones (LPT); tokens map back by rid
+            batch = sorted(batch, key=lambda r: -eng.state[r].kv.total_kv)
         pos = [eng.state[r].kv.total_kv for r in batch]
         with torch.cuda.stream(st):
             if self._graphs and len(batch) <= max(self._graphs) and self.attn_timing is None:
@@ -360,6 +367,9 @@ class PagedDecoder:
         st = dp.s_compute
         B = len(rids)
         rows_l, pos_l = list(rids), list(positions)
+        if self.lpt_order:  # the row order decode() launches with
+            order = sorted(range(B), key=lambda i: -pos_l[i])
+            rows_l, pos_l = [rows_l[i] for i in order], [pos_l[i] for i in order]
         max_ctx = max(positions) + 1
         if plan == "graph" and self._graphs:
             Bp = next(b for b in sorted(self._graphs) if b >= B)
