@@ -188,7 +188,7 @@ def run_ours(args):
                 from paper_2510_02758_b200.tp import PeerAllReduce
 
                 tp.ar = PeerAllReduce.from_group(rank, world, 8192 * configs.c4(world).model.hidden * 2,
-                                                 group=lockstep.group, device=dev)
+                                                 group=lockstep.group, device=dev, max_ctas=8 if one_gpu else 0)
         c2 = configs.c4(world)
         tr = _trace_for_rank(0, 1, args.arrivals)
         if world > 1 and args.graphs and one_gpu:

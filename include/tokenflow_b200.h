@@ -356,6 +356,10 @@ double tf_host_glibc_exp(double x);
  * tf_ar_create   this rank's communicator on the current device: a cudaMalloc'ed
  *                data buffer of capacity_bytes (the rank's GEMM partial goes
  *                there: tf_ar_buffer) + a zeroed control block (barrier flags).
+ *                max_ctas caps the grid (0 = one CTA per SM, 148); every rank
+ *                must pass the same value.  A small cap keeps the spinning
+ *                CTAs from starving the other ranks' kernels when several
+ *                ranks share ONE device (tests).
  * tf_ar_export   128 bytes: IPC handles of the data buffer and control block.
  * tf_ar_open     all_handles = world x 128 bytes in rank order: maps every
  *                peer's buffer and control block (cudaIpcOpenMemHandle; P2P
@@ -369,7 +373,7 @@ double tf_host_glibc_exp(double x);
  *                sequence of calls with the same rows; graph-capturable.
  * tf_ar_status   1 if a barrier wait timed out (10 s) since creation, else 0 (syncs).
  */
-int tf_ar_create(int32_t rank, int32_t world, int64_t capacity_bytes, int64_t* out_handle);
+int tf_ar_create(int32_t rank, int32_t world, int64_t capacity_bytes, int32_t max_ctas, int64_t* out_handle);
 void* tf_ar_buffer(int64_t ar);
 void* tf_ar_ctl(int64_t ar);
 int tf_ar_export(int64_t ar, void* out128);

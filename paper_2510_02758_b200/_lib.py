@@ -145,7 +145,7 @@ SIGNATURES = {
                                      C.c_double, _PI32, _PI32, _P]),
     "tf_select_batch": (C.c_int, [_I64, C.POINTER(TfPrio), _I32, C.c_double, _I32, C.POINTER(C.c_uint8), _P]),
     "tf_host_glibc_exp": (C.c_double, [C.c_double]),
-    "tf_ar_create": (C.c_int, [_I32, _I32, _I64, C.POINTER(_I64)]),
+    "tf_ar_create": (C.c_int, [_I32, _I32, _I64, _I32, C.POINTER(_I64)]),
     "tf_ar_buffer": (_P, [_I64]),
     "tf_ar_ctl": (_P, [_I64]),
     "tf_ar_export": (C.c_int, [_I64, _P]),

@@ -51,6 +51,7 @@ struct ArCtl {
 
 struct ArComm {
   int rank = 0, world = 1, device = 0;
+  int max_ctas = kArMaxCtas;  // grid cap (identical on every rank)
   int64_t capacity = 0;  // bytes of the data buffer
   void* data = nullptr;  // this rank's registered buffer (cudaMalloc: IPC-exportable)
   ArCtl* ctl = nullptr;
@@ -223,13 +224,16 @@ using namespace tf;
 
 extern "C" {
 
-int tf_ar_create(int32_t rank, int32_t world, int64_t capacity_bytes, int64_t* out_handle) {
+int tf_ar_create(int32_t rank, int32_t world, int64_t capacity_bytes, int32_t max_ctas, int64_t* out_handle) {
   TF_CHECK_ARG(out_handle, "tf_ar_create: out_handle is NULL");
   TF_CHECK_ARG(world >= 1 && world <= kArMaxRanks && rank >= 0 && rank < world, "tf_ar_create: rank %d of %d",
                rank, world);
   TF_CHECK_ARG(capacity_bytes > 0 && capacity_bytes % 16 == 0, "tf_ar_create: bad capacity %lld",
                (long long)capacity_bytes);
+  TF_CHECK_ARG(max_ctas >= 0 && max_ctas <= kArMaxCtas, "tf_ar_create: max_ctas %d not in [0, %d]", max_ctas,
+               kArMaxCtas);
   auto c = std::make_unique<ArComm>();
+  c->max_ctas = max_ctas ? max_ctas : kArMaxCtas;
   c->rank = rank;
   c->world = world;
   c->capacity = capacity_bytes;
@@ -329,7 +333,7 @@ int tf_ar_residual_rmsnorm(int64_t h, void* x, const void* gamma, void* h_out, i
   a.gamma = (const uint16_t*)gamma;
   a.h_out = (uint16_t*)h_out;
   a.eps = eps;
-  const int grid = rows < kArMaxCtas ? rows : kArMaxCtas;
+  const int grid = rows < c->max_ctas ? rows : c->max_ctas;
   ar_residual_rmsnorm_kernel<<<grid, kArThreads, 0, (cudaStream_t)stream>>>(a);
   TF_LAUNCH_CHECK();
   return TF_OK;

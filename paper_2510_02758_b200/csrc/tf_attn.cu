@@ -631,11 +631,16 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
   const int64_t koff = (((int64_t)a.layer * 2 + 0) * a.kv_heads + kvh) * tile;
   const int64_t voff = (((int64_t)a.layer * 2 + 1) * a.kv_heads + kvh) * tile;
   const int32_t* trow = a.table + (int64_t)a.rows[b] * a.stride;
+  // the warp's first 32 table entries in one coalesced load (lane i: block i),
+  // so the pipeline prologue waits for one table load instead of S - 1
+  // dependent ones
+  const int tab_pre = lane < nmine ? __ldg(trow + blk_lo + warp + lane * kV3Warps) : 0;
 
   auto issue = [&](int j) {  // warp-local block j -> stage j % S
     if (j < nmine) {
       const int blk = blk_lo + warp + j * kV3Warps;
-      const int64_t base = (int64_t)__ldg(trow + blk) * a.block_elems;
+      const int ent = j < 32 ? __shfl_sync(0xffffffffu, tab_pre, j) : __ldg(trow + blk);
+      const int64_t base = (int64_t)ent * a.block_elems;
       uint16_t* ks = ring + (j % S) * 2 * kTileElems;
       uint16_t* vs = ks + kTileElems;
 #pragma unroll

@@ -106,13 +106,13 @@ class PeerAllReduce:
     backend; gloo works).  Ranks living in one process (tests) are linked
     with ``PeerAllReduce.link`` instead."""
 
-    def __init__(self, rank: int, world: int, capacity_bytes: int, device=None):
+    def __init__(self, rank: int, world: int, capacity_bytes: int, device=None, max_ctas: int = 0):
         from . import _lib
 
         self._lib = _lib
         self.rank, self.world, self.capacity = rank, world, int(capacity_bytes)
         h = _lib.C.c_int64()
-        _lib.check(_lib.lib.tf_ar_create(rank, world, self.capacity, _lib.C.byref(h)), "tf_ar_create")
+        _lib.check(_lib.lib.tf_ar_create(rank, world, self.capacity, max_ctas, _lib.C.byref(h)), "tf_ar_create")
         self.handle = h.value
         ptr = _lib.lib.tf_ar_buffer(self.handle)
 
@@ -124,8 +124,9 @@ class PeerAllReduce:
         self._buf = self._buf.view(torch.bfloat16)
 
     @classmethod
-    def from_group(cls, rank: int, world: int, capacity_bytes: int, group=None, device=None) -> "PeerAllReduce":
-        self = cls(rank, world, capacity_bytes, device)
+    def from_group(cls, rank: int, world: int, capacity_bytes: int, group=None, device=None,
+                   max_ctas: int = 0) -> "PeerAllReduce":
+        self = cls(rank, world, capacity_bytes, device, max_ctas)
         C = self._lib.C
         mine = (C.c_uint8 * 128)()
         self._lib.check(self._lib.lib.tf_ar_export(self.handle, mine), "tf_ar_export")

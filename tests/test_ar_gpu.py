@@ -21,7 +21,9 @@ pytestmark = pytest.mark.gpu
 def _ranks(world, cap, cuda):
     from paper_2510_02758_b200.tp import PeerAllReduce
 
-    ars = [PeerAllReduce(r, world, cap, device=cuda) for r in range(world)]
+    # same-process ranks share the GPU: a few CTAs each, so a waiting rank
+    # never holds the SMs another rank's GEMM needs
+    ars = [PeerAllReduce(r, world, cap, device=cuda, max_ctas=8) for r in range(world)]
     PeerAllReduce.link(ars)
     return ars
 
@@ -73,8 +75,6 @@ def _run_ranks(ars, fn):
         raise errs[0]
 
 
-# world x min(rows, 148) CTAs of the same-process ranks must fit on the one
-# GPU at once (they wait for each other); on a TP run every rank has its own
 @pytest.mark.parametrize("world,rows,dim", [(2, 1, 256), (2, 128, 4096), (4, 64, 5120), (8, 24, 5120),
                                             (2, 300, 5120), (2, 17, 8192)])
 def test_fused_allreduce_residual_rmsnorm_bit_exact(cuda, world, rows, dim):
@@ -139,9 +139,11 @@ def test_rejects_bad_arguments(cuda):
     with pytest.raises(ValueError):
         check(lib.tf_ar_residual_rmsnorm(ars[0].handle, C.c_void_p(x.data_ptr()), None, None, 1, 12, 1e-6, None))
     with pytest.raises(ValueError):
-        check(lib.tf_ar_create(2, 2, 1024, C.byref(C.c_int64())))
+        check(lib.tf_ar_create(2, 2, 1024, 0, C.byref(C.c_int64())))
     with pytest.raises(ValueError):
-        check(lib.tf_ar_create(0, 9, 1024, C.byref(C.c_int64())))
+        check(lib.tf_ar_create(0, 9, 1024, 0, C.byref(C.c_int64())))
+    with pytest.raises(ValueError):
+        check(lib.tf_ar_create(0, 2, 1024, 149, C.byref(C.c_int64())))
 
 
 def test_graph_replays_advance_the_barrier(cuda):
@@ -204,7 +206,8 @@ def test_tp2_decoder_on_peer_path(cuda):
     def tp2(peer):
         shared = {"buf": [None, None], "bar": threading.Barrier(2)}
         shards = []
-        ars = [PeerAllReduce(r, 2, 4096 * shape.hidden * 2, device=cuda) for r in range(2)] if peer else None
+        ars = ([PeerAllReduce(r, 2, 4096 * shape.hidden * 2, device=cuda, max_ctas=8) for r in range(2)]
+               if peer else None)
         if peer:
             PeerAllReduce.link(ars)
         for r in range(2):
@@ -259,7 +262,7 @@ def _ipc_worker(rank, port, q):
     from paper_2510_02758_b200.tp import PeerAllReduce
 
     rows, dim, eps = 64, 1024, 1e-6
-    ar = PeerAllReduce.from_group(rank, 2, rows * dim * 2, device=torch.device("cuda", 0))
+    ar = PeerAllReduce.from_group(rank, 2, rows * dim * 2, device=torch.device("cuda", 0), max_ctas=8)
     gamma = torch.ones(dim, device="cuda", dtype=torch.bfloat16)
     res = []
     for it in range(3):
