@@ -49,9 +49,9 @@ extern "C" {
 #define TF_TIER_GPU 0
 #define TF_TIER_HOST 1
 #define TF_ENGINE_SM 0 /* SM-driven zero-copy gather/scatter kernel */
-#define TF_ENGINE_CE 1 /* copy engines (one cudaMemcpyAsync per maximal contiguous run) */
+#define TF_ENGINE_CE 1 /* copy engines (= TF_ENGINE_CE2D since ABI v1.1) */
 #define TF_ENGINE_AUTO 2 /* = TF_ENGINE_CE2D (kept for callers of ABI v1) */
-#define TF_ENGINE_CE2D 3 /* copy engines only: whole blocks batched, each partial block one 2-D copy */
+#define TF_ENGINE_CE2D 3 /* copy engines only: whole blocks as merged 1-D runs, each partial block one 2-D copy */
 
 const char* tf_last_error(void);
 int tf_abi_version(void);

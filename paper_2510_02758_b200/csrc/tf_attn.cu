@@ -1214,7 +1214,11 @@ static int sm_count() {
 
 static int64_t v4_kmax(int max_ctx) { return (std::max(1, (max_ctx + kBlk - 1) / kBlk) + kPerMin - 1) / kPerMin + 1; }
 
-static int64_t v4_counter_bytes(int B, int kv) { return ((int64_t)B * kv * 4 + 255) / 256 * 256; }
+// fixed size (the largest batch), for the same reason as attn5_counter_bytes
+static int64_t v4_counter_bytes(int B, int kv) {
+  (void)B;
+  return ((int64_t)kV4MaxB * kv * 4 + 255) / 256 * 256;
+}
 
 template <int D, int G>
 static int launch(const AttnArgs& a, int B, cudaStream_t st) {

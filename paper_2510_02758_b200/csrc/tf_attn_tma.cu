@@ -624,8 +624,16 @@ int64_t attn5_kmax(int max_ctx) {
   return (std::max(1, (max_ctx + kBlk5 - 1) / kBlk5) + kAttn5MinPer - 1) / kAttn5MinPer + 1;
 }
 
-// workspace: [ticket u64 | pad to 256][merge counters B*kv int32, to 256][(max, sum) partials][acc partials]
-int64_t attn5_counter_bytes(int B, int kv) { return 256 + ((int64_t)B * kv * 4 + 255) / 256 * 256; }
+// workspace: [ticket u64 | pad to 256][merge counters kAttn5MaxB*kv int32, to 256][(max, sum) partials][acc partials]
+// The counter region has a FIXED size (the largest batch), independent of this
+// launch's B: the counters must read zero at every launch, and the mergers
+// reset only the ones they used - if the region grew with B, a larger batch
+// would find the previous launch's partials where its counters are and wait
+// for a count that never comes.
+int64_t attn5_counter_bytes(int B, int kv) {
+  (void)B;
+  return 256 + ((int64_t)kAttn5MaxB * kv * 4 + 255) / 256 * 256;
+}
 
 int64_t attn5_workspace(const Pool* p, int B, int max_ctx, int G) {
   return attn5_counter_bytes(B, p->kv_heads) +

@@ -11,12 +11,12 @@
 //                   of outstanding sysmem loads (h2d).  Grid capped to a few
 //                   dozen CTAs: PCIe, not the SMs, is the bound, and the
 //                   decode step keeps the rest of the machine.
-//   TF_ENGINE_CE  - copy engines: the segments are coalesced into maximal
-//                   contiguous runs (a whole block of all layers is a single
-//                   2 MiB run in this layout, LIFO-adjacent blocks merge into
-//                   longer ones), one cudaMemcpyAsync per run; no SM is used.
-//   TF_ENGINE_CE2D - copy engines only: whole blocks as above, every partial
-//                   block as ONE 2-D copy (its runs are equally spaced).
+//   TF_ENGINE_CE / CE2D / AUTO - copy engines only: whole blocks (all
+//                   layers) are coalesced into maximal contiguous runs (a
+//                   whole block is a single 2 MiB run in this layout, LIFO-
+//                   adjacent blocks merge into longer ones), one cudaMemcpyAsync
+//                   per run; every partial block is ONE 2-D copy (its runs are
+//                   equally spaced).  No SM is used.
 #include <algorithm>
 
 #include "tf_common.cuh"
@@ -225,8 +225,9 @@ static int swap_entry(int64_t pool, const tf_seg* segs, int32_t n, int32_t l0, i
   }
   if (n == 0) return TF_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  if (engine == TF_ENGINE_CE) return swap_ce(*p, segs, n, l0, l1, to_host, st);
-  if (engine == TF_ENGINE_CE2D || engine == TF_ENGINE_AUTO) {
+  if (engine == TF_ENGINE_CE || engine == TF_ENGINE_CE2D || engine == TF_ENGINE_AUTO) {
+    // (TF_ENGINE_CE used to move a partial block as 2 x kv_heads x layers
+    // separate 1-D runs; one submission each made it ~100x slower than this)
     // whole blocks (all layers): merged 1-D runs; every other
     // segment: one 2-D copy each.  No SM is used at all (the copy engines
     // beat the SM kernel at every chunk size, profiles/r2_wt_chunks_ce2d.json,
