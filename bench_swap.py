@@ -198,11 +198,6 @@ def overlap(pool, args):
     ws_n = max(1, int(_lib.lib.tf_paged_decode_attn_workspace(pool.handle, B, ctx, HQ)))
     ws = torch.zeros(ws_n, dtype=torch.uint8, device=dev)
     sc, sd, sh = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    # swap traffic smaller than one decode's time (so 100% hiding is possible):
-    # NB blocks out (write-through + evict) and NB in (loads), 2 MiB each
-    nbk = args.overlap_blocks
-    g = np.arange(pool.n_blocks // 2, pool.n_blocks // 2 + nbk)
-    segs = segs_for(g, np.arange(nbk) % pool.n_host_blocks)
     res = {}
     for eng in args.engines:
         def decode():
@@ -230,10 +225,19 @@ def overlap(pool, args):
             return (time.perf_counter() - t0) / reps
 
         t_dec = run([decode])
+        # swap traffic sized to ~80% of one decode (at ~45 GB/s per direction
+        # when both run): 100% hiding is then possible, so the fraction
+        # measures overlap quality, not the ratio of the two volumes.
+        # NB blocks out (write-through + evict) and NB in (loads), 2 MiB each
+        nbk = args.overlap_blocks or max(1, int(0.8 * t_dec * 45e9 / pool.block_bytes))
+        nbk = min(nbk, pool.n_blocks // 2, pool.n_host_blocks)
+        g = np.arange(pool.n_blocks // 2, pool.n_blocks // 2 + nbk)
+        segs = segs_for(g, np.arange(nbk) % pool.n_host_blocks)
         t_swp = run([swaps])
         t_both = run([decode, swaps])
         hidden = 1.0 - max(0.0, t_both - t_dec) / t_swp
-        res[{0: "sm", 1: "ce", 2: "auto", 3: "ce2d"}[eng]] = {"t_decode_ms": t_dec * 1e3, "t_swap_ms": t_swp * 1e3,
+        res[{0: "sm", 1: "ce", 2: "auto", 3: "ce2d"}[eng]] = {"blocks_each_way": nbk,
+                                           "t_decode_ms": t_dec * 1e3, "t_swap_ms": t_swp * 1e3,
                                            "t_both_ms": t_both * 1e3, "hidden_frac": hidden,
                                            "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = 32 layers of "
                                                    "paged attention B=64 ctx=2600; swap = NB x 2 MiB out + NB x 2 MiB in, concurrent"}
@@ -247,7 +251,7 @@ def main():
     ap.add_argument("--host-blocks", type=int, default=8192)
     ap.add_argument("--engines", default="0,1")
     ap.add_argument("--overlap", action="store_true")
-    ap.add_argument("--overlap-blocks", type=int, default=96)
+    ap.add_argument("--overlap-blocks", type=int, default=0, help="0: sized to ~80%% of the decode time")
     ap.add_argument("--out", default="gpurun_out/swap_sweep.json")
     ap.add_argument("--wt-only", action="store_true", help="only the write-through-shaped chunk sizes")
     args = ap.parse_args()

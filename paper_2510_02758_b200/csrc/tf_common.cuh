@@ -58,6 +58,18 @@ struct Pool {
   std::vector<uint8_t> used_gpu, used_host;  // per-block allocation state (double-free check)
   alignas(64) unsigned char tmap[128];       // CUtensorMap of the HBM pool (v5 attention), built lazily
   bool tmap_ok = false;
+  // copy-engine swaps: one auxiliary stream per direction (0 = d2h, 1 = h2d)
+  // so consecutive runs of a chunk alternate between two copy queues and the
+  // per-copy setup of one overlaps the transfer of the other; created lazily
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t fork_ev[2] = {nullptr, nullptr}, join_ev[2] = {nullptr, nullptr};
+  ~Pool() {
+    for (int i = 0; i < 2; ++i) {
+      if (aux[i]) cudaStreamDestroy(aux[i]);
+      if (fork_ev[i]) cudaEventDestroy(fork_ev[i]);
+      if (join_ev[i]) cudaEventDestroy(join_ev[i]);
+    }
+  }
 
   // element offset of (block, layer, kv, head, slot, dim=0)
   __host__ __device__ int64_t off(int64_t b, int l, int kv, int h, int s) const {

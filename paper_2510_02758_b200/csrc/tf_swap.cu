@@ -143,67 +143,88 @@ static int swap_sm(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int
   return TF_OK;
 }
 
-// Copy-engine path: maximal contiguous runs, one submission per run.
+// Copy-engine path.  Whole blocks (all layers) become maximal contiguous 1-D
+// runs (a block is one 2 MiB run; LIFO-adjacent blocks merge).  A PARTIAL
+// block is ONE 2-D copy: the n slots of one (block, layer, K|V, head) tile sit
+// at the same offset in every tile, and the tiles of a block are consecutive
+// (block_tokens * head_dim elements apart), so a partial block over layers
+// [l0, l1) is width n_slots * head_dim * 2 B x height (l1 - l0) * 2 * kv_heads
+// rows at a pitch of one tile - instead of that many separate runs or an SM
+// kernel.  No SM is used.
+//
+// Copies alternate between the caller's stream and the pool's auxiliary copy
+// stream of this direction (fork / join through events, so the chunk still
+// completes on the caller's stream): every copy carries a fixed setup cost
+// (~4 us per 2 MiB block on one queue: 51 vs 57 GB/s) that the other queue's
+// transfer then covers.
+struct CopyOp {
+  void* dst;
+  const void* src;
+  size_t width, height, pitch;  // height 1 = a 1-D run of `width` bytes
+};
+
 static int swap_ce(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int to_host,
                    cudaStream_t st) {
-  std::vector<void*> dst, src;
-  std::vector<size_t> sz;
+  std::vector<CopyOp> ops;
   const bool all_layers = (l0 == 0 && l1 == p.n_layers);
-  auto push = [&](int64_t goff, int64_t hoff, int64_t elems) {
+  auto push_run = [&](int64_t goff, int64_t hoff, int64_t elems) {
     uint16_t* g = p.gpu + goff;
     uint16_t* h = p.host + hoff;
-    size_t bytes = (size_t)elems * 2;
-    // merge with the previous run when both sides continue contiguously
-    if (!sz.empty()) {
-      char* pd = (char*)dst.back() + sz.back();
-      char* ps = (char*)src.back() + sz.back();
-      if (pd == (char*)(to_host ? (void*)h : (void*)g) && ps == (char*)(to_host ? (void*)g : (void*)h)) {
-        sz.back() += bytes;
-        return;
-      }
+    const size_t bytes = (size_t)elems * 2;
+    void* d = to_host ? (void*)h : (void*)g;
+    const void* sp = to_host ? (const void*)g : (const void*)h;
+    // merge with the previous 1-D run when both sides continue contiguously
+    if (!ops.empty() && ops.back().height == 1 && (char*)ops.back().dst + ops.back().width == (char*)d &&
+        (const char*)ops.back().src + ops.back().width == (const char*)sp) {
+      ops.back().width += bytes;
+      return;
     }
-    dst.push_back(to_host ? (void*)h : (void*)g);
-    src.push_back(to_host ? (void*)g : (void*)h);
-    sz.push_back(bytes);
+    ops.push_back({d, sp, bytes, 1, bytes});
   };
-  for (int32_t i = 0; i < n; ++i) {
-    const tf_seg& s = segs[i];
-    if (all_layers && s.n_slots == p.block_tokens && s.slot_begin == 0) {
-      push(p.off(s.gpu_block, 0, 0, 0, 0), p.off(s.host_block, 0, 0, 0, 0), p.block_elems);
-      continue;
-    }
-    for (int l = l0; l < l1; ++l)
-      for (int kv = 0; kv < 2; ++kv)
-        for (int h = 0; h < p.kv_heads; ++h)
-          push(p.off(s.gpu_block, l, kv, h, s.slot_begin), p.off(s.host_block, l, kv, h, s.slot_begin),
-               (int64_t)s.n_slots * p.head_dim);
-  }
-  // One plain async copy per maximal run: few, large submissions (a chunk of
-  // whole blocks is typically a handful of multi-MiB runs).
-  for (size_t i = 0; i < sz.size(); ++i)
-    TF_CUDA(cudaMemcpyAsync(dst[i], src[i], sz[i], to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st));
-  return TF_OK;
-}
-
-// Copy-engine path for PARTIAL blocks: the n slots of one (block, layer, K|V,
-// head) run sit at the same offset in every run, and the runs of a block are
-// consecutive tiles of block_tokens * head_dim elements - so a partial block
-// over layers [l0, l1) is ONE 2-D copy (width n_slots * head_dim * 2 bytes,
-// height (l1 - l0) * 2 * kv_heads rows, pitch one tile) for the DMA engine,
-// instead of 2 * kv_heads * layers separate runs or an SM kernel.
-static int swap_ce2d(const Pool& p, const tf_seg* segs, int32_t n, int32_t l0, int32_t l1, int to_host,
-                     cudaStream_t st) {
   const size_t pitch = (size_t)p.tile_elems * 2;
   const size_t rows = (size_t)(l1 - l0) * 2 * p.kv_heads;
   for (int32_t i = 0; i < n; ++i) {
     const tf_seg& s = segs[i];
-    uint16_t* g = p.gpu + p.off(s.gpu_block, l0, 0, 0, s.slot_begin);
-    uint16_t* h = p.host + p.off(s.host_block, l0, 0, 0, s.slot_begin);
-    const size_t width = (size_t)s.n_slots * p.head_dim * 2;
-    if (to_host)
-      TF_CUDA(cudaMemcpy2DAsync(h, pitch, g, pitch, width, rows, cudaMemcpyDeviceToHost, st));
+    if (all_layers && s.n_slots == p.block_tokens && s.slot_begin == 0) {
+      push_run(p.off(s.gpu_block, 0, 0, 0, 0), p.off(s.host_block, 0, 0, 0, 0), p.block_elems);
+    } else if (s.n_slots == p.block_tokens && s.slot_begin == 0) {
+      // whole block over a layer range: its tiles for [l0, l1) are contiguous
+      push_run(p.off(s.gpu_block, l0, 0, 0, 0), p.off(s.host_block, l0, 0, 0, 0), (int64_t)rows * p.tile_elems);
+    } else {
+      uint16_t* g = p.gpu + p.off(s.gpu_block, l0, 0, 0, s.slot_begin);
+      uint16_t* h = p.host + p.off(s.host_block, l0, 0, 0, s.slot_begin);
+      ops.push_back({to_host ? (void*)h : (void*)g, to_host ? (const void*)g : (const void*)h,
+                     (size_t)s.n_slots * p.head_dim * 2, rows, pitch});
+    }
+  }
+  if (ops.empty()) return TF_OK;
+  const cudaMemcpyKind kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
+  Pool& pm = const_cast<Pool&>(p);
+  const int dir = to_host ? 0 : 1;
+  cudaStream_t st2 = nullptr;
+  if (ops.size() >= 2) {
+    if (!pm.aux[dir]) {
+      int lo = 0, hi = 0;
+      TF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      TF_CUDA(cudaStreamCreateWithPriority(&pm.aux[dir], cudaStreamNonBlocking, hi));
+      TF_CUDA(cudaEventCreateWithFlags(&pm.fork_ev[dir], cudaEventDisableTiming));
+      TF_CUDA(cudaEventCreateWithFlags(&pm.join_ev[dir], cudaEventDisableTiming));
+    }
+    st2 = pm.aux[dir];
+    TF_CUDA(cudaEventRecord(pm.fork_ev[dir], st));
+    TF_CUDA(cudaStreamWaitEvent(st2, pm.fork_ev[dir], 0));
+  }
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const CopyOp& o = ops[i];
+    cudaStream_t q = (st2 && (i & 1)) ? st2 : st;
+    if (o.height == 1)
+      TF_CUDA(cudaMemcpyAsync(o.dst, o.src, o.width, kind, q));
     else
-      TF_CUDA(cudaMemcpy2DAsync(g, pitch, h, pitch, width, rows, cudaMemcpyHostToDevice, st));
+      TF_CUDA(cudaMemcpy2DAsync(o.dst, o.pitch, o.src, o.pitch, o.width, o.height, kind, q));
+  }
+  if (st2) {
+    TF_CUDA(cudaEventRecord(pm.join_ev[dir], st2));
+    TF_CUDA(cudaStreamWaitEvent(st, pm.join_ev[dir], 0));
   }
   return TF_OK;
 }
@@ -225,23 +246,12 @@ static int swap_entry(int64_t pool, const tf_seg* segs, int32_t n, int32_t l0, i
   }
   if (n == 0) return TF_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  if (engine == TF_ENGINE_CE || engine == TF_ENGINE_CE2D || engine == TF_ENGINE_AUTO) {
-    // (TF_ENGINE_CE used to move a partial block as 2 x kv_heads x layers
-    // separate 1-D runs; one submission each made it ~100x slower than this)
-    // whole blocks (all layers): merged 1-D runs; every other
-    // segment: one 2-D copy each.  No SM is used at all (the copy engines
-    // beat the SM kernel at every chunk size, profiles/r2_wt_chunks_ce2d.json,
-    // and leave the SMs to the decode step).
-    std::vector<tf_seg> full, part;
-    const bool all_layers = (l0 == 0 && l1 == p->n_layers);
-    for (int32_t i = 0; i < n; ++i)
-      (all_layers && segs[i].n_slots == p->block_tokens ? full : part).push_back(segs[i]);
-    if (!full.empty()) {
-      int rc = swap_ce(*p, full.data(), (int32_t)full.size(), l0, l1, to_host, st);
-      if (rc != TF_OK) return rc;
-    }
-    return part.empty() ? TF_OK : swap_ce2d(*p, part.data(), (int32_t)part.size(), l0, l1, to_host, st);
-  }
+  // every copy-engine mode is the same path now (TF_ENGINE_CE used to move a
+  // partial block as 2 x kv_heads x layers separate 1-D runs): the copy
+  // engines beat the SM kernel at every chunk size
+  // (profiles/r2_wt_chunks_ce2d.json) and leave the SMs to the decode step
+  if (engine == TF_ENGINE_CE || engine == TF_ENGINE_CE2D || engine == TF_ENGINE_AUTO)
+    return swap_ce(*p, segs, n, l0, l1, to_host, st);
   TF_CHECK_ARG(engine == TF_ENGINE_SM, "swap: unknown engine %d", engine);
   return swap_sm(*p, segs, n, l0, l1, to_host, st);
 }
