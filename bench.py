@@ -538,9 +538,8 @@ def _aggregate(local, world, tp_mode, device):
 
 def _swap_block(agg, engine):
     sw = {"d2h_tokens": agg["d2h_tok"], "h2d_tokens": agg["h2d_tok"], "chunks": agg["chunks"],
-          "engine": {0: "SM kernel", 1: "copy-engine batch (1-D runs)",
-                     2: "copy engines (whole blocks batched, partial blocks as 2-D copies)",
-                     3: "copy engines (whole blocks batched, partial blocks as 2-D copies)"}[engine],
+          "engine": "SM kernel" if engine == 0 else
+                    "copy engines (whole blocks as merged 1-D runs, partial blocks as 2-D copies, two copy queues)",
           "d2h_gbs": agg["d2h_gbs"], "h2d_gbs": agg["h2d_gbs"], "pcie_gen5_gbs": PCIE_GEN5_GBS}
     for k in ("d2h", "h2d"):
         if sw[f"{k}_gbs"]:
@@ -550,12 +549,12 @@ def _swap_block(agg, engine):
 
 def _attn_kernel_name(shape, batch, graphs):
     """The decode-attention implementation the library picks for this launch
-    (tf_paged_decode_attn_impl default: v5 for B <= 64, v3 above)."""
+    (tf_paged_decode_attn_impl default: v3 at every batch)."""
     G = shape.n_q_heads // shape.n_kv_heads
     env = os.environ.get("TF_ATTN_IMPL", "")[:1]
     impl = int(env) if env in ("1", "2", "3", "4", "5") else 0
     if impl == 0:
-        impl = 5 if batch <= 64 else 3
+        impl = 3
     return {1: "paged_attn_kernel (v1, CUDA cores)", 2: "paged_attn_tma_kernel (v2, bulk copy)",
             3: f"paged_attn_mma_kernel<{G}> (v3, split-KV cp.async + mma.sync) + combine",
             4: f"paged_attn_stream_kernel<{G}> (v4 stream-K)",
@@ -880,8 +879,8 @@ def main():
     # pinned host tier: 16384 x 2 MiB = 32 GiB covers the timed window; a
     # full run of the burst peaks near 22K blocks (replay of the same trace)
     ap.add_argument("--host-blocks", type=int, default=int(os.environ.get("TF_HOST_BLOCKS", 0)))
-    ap.add_argument("--swap-engine", type=int, default=2, help="0 SM kernel, 1 copy engines (1-D runs), 2 copy "
-                    "engines (whole blocks batched, each partial block one 2-D copy)")
+    ap.add_argument("--swap-engine", type=int, default=2, help="0 SM kernel; 1, 2 or 3 copy engines (whole blocks as "
+                    "merged 1-D runs, each partial block one 2-D copy, alternated over two copy queues)")
     ap.add_argument("--arrivals", default="burst", choices=["burst", "poisson"])
     ap.add_argument("--config", default="c2", choices=["c2", "c4"], help="c2: Llama3-8B replicas (C2/C3, default); "
                     "c4: Qwen2.5-32B tensor-parallel over the launched ranks")

@@ -170,9 +170,11 @@ int tf_q_fill_synthetic(void* q, const int32_t* dev_rids, const int32_t* dev_pos
  * 16-token K/V tiles with TMA tensor loads (128-B swizzle) into a per-warp
  * mbarrier ring, running ahead across (request, head) boundaries; a (request,
  * head) shared by several warps is merged in-kernel.  v3 (head_dim 128) is a
- * split-KV grid of (request, kv head, split) CTAs with cp.async rings.  The
- * default picks v5 for B <= 64 and v3 above (faster there on B200); other
- * shapes use the CUDA-core kernels.
+ * split-KV grid of (request, kv head, split) CTAs with cp.async rings and is
+ * the default at every batch (2-stage rings at B <= 96, 3 above); v5 is
+ * opt-in (impl 5): its waits are bounded (2 s; an expired wait is counted in
+ * workspace bytes [8, 64) instead of hanging the GPU).  Other shapes use the
+ * CUDA-core / bulk-copy kernels.
  * max_ctx must bound every ctx[b].  The workspace (size from
  * tf_paged_decode_attn_workspace for the same B / max_ctx / n_q_heads, under
  * the same implementation) must be ZERO-filled before its first use; every

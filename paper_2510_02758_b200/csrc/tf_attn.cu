@@ -1148,9 +1148,13 @@ static int attn_impl_sel() {
   return g_impl;
 }
 static thread_local int g_cur_b = 0;  // batch of the launch being planned (for the "by batch" default)
+// default: v3 at every batch.  v5 (TMA + stream-K, TF_ATTN_IMPL=5) is within
+// a few percent of v3 where measured (profiles/r2_attn_v3_v5.json) but its
+// in-kernel merge stalled the full-size C2 replay (tiny shapes, ragged B <= 64;
+// its waits are now bounded, tests/attn_parity.py), so it stays opt-in
 static int attn_impl() {
   const int i = attn_impl_sel();
-  return i ? i : (g_cur_b <= 64 ? 5 : 3);
+  return i ? i : 3;
 }
 
 // test-only fault injection (TF_ATTN_MUTATE=1: every (request, kv head) with
@@ -1165,13 +1169,17 @@ static int attn_mutate() {
   return m;
 }
 
+// v3 ring depth: 2 stages (3 CTAs = 12 warps per SM) at B <= 96, 3 stages
+// (2 CTAs, 8 warps) above: at B = 64 the extra resident warps win 4-5% at
+// C2-live contexts, at B = 128 the two are equal (profiles/r2_attn_lpt_stages.json).
+// TF_ATTN_STAGES=2|3 forces one.
 static int v3_stages() {
   static int st = -1;
   if (st < 0) {
     const char* e = getenv("TF_ATTN_STAGES");
-    st = (e && e[0] == '2') ? 2 : 3;
+    st = (e && (e[0] == '2' || e[0] == '3')) ? e[0] - '0' : 0;
   }
-  return st;
+  return st ? st : (g_cur_b <= 96 ? 2 : 3);
 }
 
 static int g_minblk = 8;

@@ -57,16 +57,47 @@ __device__ __forceinline__ void mbar_init5(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx5(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait5(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ unsigned long long now5() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr unsigned long long kWait5Ns = 2000ull * 1000 * 1000;  // 2 s: a wait that long is a bug, not load
+
+// Diagnostics of a bounded wait that expired (workspace bytes [8, 64), see
+// attn5_counter_bytes): int32 [0] = number of expired waits, [2..9] = the
+// first one's (kind 1 = TMA stage / 2 = merge counter, logical CTA, warp, B,
+// segment, observed, expected, iteration).  The kernel then continues with
+// whatever the buffer holds - wrong output instead of a hung GPU.
+__device__ __forceinline__ void wait5_expired(int* diag, int kind, int lid, int warp, int B, int sid, int seen,
+                                              int want, int it) {
+  if (atomicAdd(diag, 1) == 0) {
+    int* r = diag + 2;
+    r[0] = kind; r[1] = lid; r[2] = warp; r[3] = B; r[4] = sid; r[5] = seen; r[6] = want; r[7] = it;
+    __threadfence();
+  }
+}
+
+__device__ __forceinline__ bool mbar_try5(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "W5_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra W5_%=;\n"
-      "}\n" ::"r"(s_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(s_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// true when the phase completed; false after kWait5Ns
+__device__ __forceinline__ bool mbar_wait5(uint64_t* bar, uint32_t parity) {
+  if (mbar_try5(bar, parity)) return true;
+  const unsigned long long t0 = now5();
+  while (!mbar_try5(bar, parity))
+    if (now5() - t0 > kWait5Ns) return false;
+  return true;
 }
 __device__ __forceinline__ void ldsm4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -384,9 +415,17 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
     // wait until the cnt - 1 lower pieces are published (acquire), then merge
     if (lane == 0) {
       unsigned int v = 0;
-      do {
+      unsigned long long t0 = 0;
+      for (;;) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.counters + mrg_sid) : "memory");
-      } while ((int)v != mrg_cnt - 1);
+        if ((int)v == mrg_cnt - 1) break;
+        if (!t0) {
+          t0 = now5();
+        } else if (now5() - t0 > kWait5Ns) {
+          wait5_expired(a.diag, 2, lid_sh, warp, B, mrg_sid, (int)v, mrg_cnt - 1, n);
+          break;
+        }
+      }
     }
     __syncwarp();
     const int64_t slot0 = (int64_t)mrg_sid * a.kmax;
@@ -457,7 +496,8 @@ __global__ void __launch_bounds__(W * 32, CPS) paged_attn_tma5_kernel(const __gr
     if (i == pub_at) publish();
     issue(i + S - 1);
     const int s = i % S;
-    mbar_wait5(&bar[s], (uint32_t)((i / S) & 1));
+    if (!mbar_wait5(&bar[s], (uint32_t)((i / S) & 1)) && lane == 0)
+      wait5_expired(a.diag, 1, lid_sh, warp, B, -1, i % S, (i / S) & 1, i);
     const uint32_t kst = ring + s * kStage;
     const uint32_t vst = kst + NH * kHalf;
     const int blk = cc.j;
@@ -624,7 +664,8 @@ int64_t attn5_kmax(int max_ctx) {
   return (std::max(1, (max_ctx + kBlk5 - 1) / kBlk5) + kAttn5MinPer - 1) / kAttn5MinPer + 1;
 }
 
-// workspace: [ticket u64 | pad to 256][merge counters kAttn5MaxB*kv int32, to 256][(max, sum) partials][acc partials]
+// workspace: [ticket u64 | diagnostics int32[14] | pad to 256][merge counters kAttn5MaxB*kv int32, to 256]
+//            [(max, sum) partials][acc partials]
 // The counter region has a FIXED size (the largest batch), independent of this
 // launch's B: the counters must read zero at every launch, and the mergers
 // reset only the ones they used - if the region grew with B, a larger batch
@@ -652,6 +693,7 @@ int attn5_launch(Pool* p, Attn5Args a, int G, int max_ctx, void* workspace, int6
   TF_CHECK_ARG(workspace && workspace_bytes >= need, "tf_paged_decode_attn: workspace too small (%lld < %lld)",
                (long long)workspace_bytes, (long long)need);
   a.ticket = (unsigned long long*)workspace;
+  a.diag = (int*)((char*)workspace + 8);
   a.counters = (int32_t*)((char*)workspace + 256);
   a.ws_ml = (float*)((char*)workspace + cb);
   a.ws_acc = a.ws_ml + (int64_t)a.B * p->kv_heads * a.kmax * G * 2;

@@ -18,6 +18,7 @@ struct Attn5Args {
   float* ws_ml;       // [B*kv][kmax][G][2] partial (max, sum)
   int32_t* counters;  // [B*kv] self-resetting merge counters
   unsigned long long* ticket;  // dispatch-order CTA ticket (monotonic; grid size is fixed per process)
+  int* diag;                   // expired-wait diagnostics (workspace bytes [8, 64))
   int32_t stride, n_layers, kv_heads, layer, hq, B, kmax, min_per;
   float scale_log2;
   int32_t mutate;     // test-only fault injection (TF_ATTN_MUTATE), 0 in production

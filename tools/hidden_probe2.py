@@ -39,7 +39,7 @@ def main():
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--ctx", type=int, default=600)
     ap.add_argument("--tokens", type=int, default=40, help="swap tokens per step per direction")
-    ap.add_argument("--seg", type=int, default=8, help="slots per partial-block segment")
+    ap.add_argument("--seg", type=int, default=8, help="slots per partial-block segment (16 = whole blocks)")
     ap.add_argument("--engine", type=int, default=3)
     ap.add_argument("--steps", type=int, default=24)
     ap.add_argument("--out", default="gpurun_out/hidden_probe2.json")
