@@ -181,14 +181,18 @@ def run_ours(args):
             import torch.distributed as dist
 
             lockstep = Lockstep(dist.new_group(backend="gloo"))
-            if args.tp_data == "peer":
+            if args.tp_data == "peer" and not one_gpu:
+                # (the one-GPU dry run keeps the gloo data path: its ranks are
+                # processes time-slicing one device, so a peer barrier would wait
+                # a scheduling slice per all-reduce; tests/test_ar_gpu.py covers
+                # the peer kernel across processes on one GPU)
                 # data path: each rank's o_proj / down_proj partial goes into its
                 # registered buffer, one kernel reads the peers' over NVLink and
                 # fuses residual + RMSNorm (csrc/tf_ar.cu); handles over gloo
                 from paper_2510_02758_b200.tp import PeerAllReduce
 
                 tp.ar = PeerAllReduce.from_group(rank, world, 8192 * configs.c4(world).model.hidden * 2,
-                                                 group=lockstep.group, device=dev, max_ctas=8 if one_gpu else 0)
+                                                 group=lockstep.group, device=dev)
         c2 = configs.c4(world)
         tr = _trace_for_rank(0, 1, args.arrivals)
         if world > 1 and args.graphs and one_gpu:
@@ -216,6 +220,11 @@ def run_ours(args):
         profile_hooks(dp)
     if args.graphs:
         dp.enable_scratch()
+        if tp is not None and getattr(tp, "ar", None) is not None:
+            # the capture warm-up runs the peer all-reduce eagerly: start it together
+            import torch.distributed as dist
+
+            dist.barrier(group=lockstep.group)
         model.enable_graphs(dp)
     if args.policy == "fcfs":  # the paper's comparison baseline on the same data plane
         from paper_2510_02758_b200.scheduler import FcfsPolicy
@@ -381,6 +390,8 @@ def run_ours(args):
     with sampler:
         res = eng.run()
     torch.cuda.synchronize()
+    if tp is not None and getattr(tp, "ar", None) is not None and tp.ar.status() != 0:
+        raise RuntimeError("peer all-reduce: a barrier wait timed out (a rank fell > 10 s behind)")
     if state["phase"] not in ("done", "ttft", "rest"):
         raise RuntimeError(f"bench ended in phase {state['phase']} after {len(eng.steps)} steps")
     timed = state["timed"]
