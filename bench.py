@@ -644,7 +644,7 @@ def _start_watchdog(eng, dp, period):
     threading.Thread(target=loop, daemon=True).start()
 
 
-def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=24):
+def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=48, rounds=7):
     """Transfer hidden under decode: the real decode step (the
     captured Llama3-8B forward of the live batch) S times alone, the swap
     traffic alone (``blocks_out`` 2 MiB blocks gathered to pinned host on the
@@ -695,12 +695,12 @@ def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=24):
     # alternate the three measurements over several rounds and take medians:
     # a small swap volume makes the difference T_both - T_decode tiny, so
     # drift between separate runs would otherwise dominate it
-    rounds = {"dec": [], "swp": [], "both": []}
-    for _ in range(5):
-        rounds["dec"].append(run([decode]))
-        rounds["both"].append(run([decode, swaps]))
-        rounds["swp"].append(run([swaps]))
-    t_dec, t_swp, t_both = (statistics.median(rounds[k]) for k in ("dec", "swp", "both"))
+    samples = {"dec": [], "swp": [], "both": []}
+    for _ in range(rounds):
+        samples["dec"].append(run([decode]))
+        samples["both"].append(run([decode, swaps]))
+        samples["swp"].append(run([swaps]))
+    t_dec, t_swp, t_both = (statistics.median(samples[k]) for k in ("dec", "swp", "both"))
     pool.free(_lib.TIER_GPU, g)
     pool.free(_lib.TIER_HOST, h)
     return {"blocks_out_per_step": blocks_out, "blocks_in_per_step": blocks_in, "batch": len(rids),
@@ -708,10 +708,11 @@ def measure_hidden(model, dp, eng, rids, blocks_out, blocks_in, steps=24):
             "t_both_ms": round(t_both * 1e3, 3),
             "swap_gbs": round((blocks_out + blocks_in) * pool.block_bytes / t_swp / 1e9, 2),
             "hidden_frac": round(min(1.0, 1.0 - max(0.0, t_both - t_dec) / t_swp), 4),
-            "method": "median of 5 alternating rounds of 24 steps each (decode alone / both / swaps alone)"}
+            "method": f"median of {rounds} alternating rounds of {steps} steps each (decode alone / both / swaps "
+                      "alone)"}
 
 
-def measure_hidden_mix(model, dp, eng, rids, ev0, ev1, nsteps, engine, steps=24):
+def measure_hidden_mix(model, dp, eng, rids, ev0, ev1, nsteps, engine, steps=48, rounds=7):
     """Transfer hidden under decode for the window's OWN swap mix: the chunks
     the engine issued in the window (their segment shapes, one call per chunk,
     the serving engine), spread at the window's per-step density over
@@ -767,12 +768,12 @@ def measure_hidden_mix(model, dp, eng, rids, ev0, ev1, nsteps, engine, steps=24)
 
     decode()
     swaps(0)
-    rounds = {"dec": [], "swp": [], "both": []}
-    for _ in range(5):
-        rounds["dec"].append(run(True, False))
-        rounds["both"].append(run(True, True))
-        rounds["swp"].append(run(False, True))
-    t_dec, t_swp, t_both = (statistics.median(rounds[x]) for x in ("dec", "swp", "both"))
+    samples = {"dec": [], "swp": [], "both": []}
+    for _ in range(rounds):
+        samples["dec"].append(run(True, False))
+        samples["both"].append(run(True, True))
+        samples["swp"].append(run(False, True))
+    t_dec, t_swp, t_both = (statistics.median(samples[x]) for x in ("dec", "swp", "both"))
     pool.free(_lib.TIER_GPU, g)
     pool.free(_lib.TIER_HOST, h)
     toks = sum(n for _, sg in take for _, n in sg)
@@ -780,7 +781,7 @@ def measure_hidden_mix(model, dp, eng, rids, ev0, ev1, nsteps, engine, steps=24)
             "t_decode_ms": round(t_dec * 1e3, 3), "t_swap_ms": round(t_swp * 1e3, 3),
             "t_both_ms": round(t_both * 1e3, 3),
             "hidden_frac": round(min(1.0, 1.0 - max(0.0, t_both - t_dec) / t_swp), 4) if t_swp > 0 else None,
-            "method": "the window's chunks replayed at its per-step density; median of 5 alternating rounds of "
+            "method": f"the window's chunks replayed at its per-step density; median of {rounds} alternating rounds of "
                       f"{steps} steps (decode alone / both / swaps alone)"}
 
 

@@ -118,12 +118,17 @@ def test_graph_decode_matches_eager(cuda):
     assert torch.allclose(a, b, atol=3e-2, rtol=3e-2)
 
 
-def _host_mirror_mismatches(dp, eng, fused):
+def _host_mirror_mismatches(dp, eng, fused, stale=None):
     """Byte check of the host tier against HBM: every position the engine
     counts as mirrored on the host (fused: HOSTV flags set by the decode /
     prefill epilogue; reference write-through: the prefix [0, cpu_synced) of
     landed chunks, tokensim/kvstore.py:112-141) that is still LIVE in HBM must
-    hold the same bf16 bits in both tiers, for every layer / K|V / head."""
+    hold the same bf16 bits in both tiers, for every layer / K|V / head.
+
+    ``stale[rid]``: a recompute (engine.py:889-917) re-prefills [0, total_kv)
+    but keeps cpu_synced, as the reference does - the host prefix then holds
+    the decode-time KV and HBM the (numerically different, equally valid)
+    re-prefilled KV of the same tokens; those positions are not compared."""
     import numpy as np
     import torch
 
@@ -141,6 +146,8 @@ def _host_mirror_mismatches(dp, eng, fused):
             m &= (f & HOSTV) != 0
         else:
             m[s.kv.cpu_synced:] = False
+            if stale:
+                m[: stale.get(rid, 0)] = False
         pos = np.nonzero(m)[0]
         if not len(pos):
             continue
@@ -163,17 +170,30 @@ def test_host_tier_bytes_equal_hbm_during_serving(cuda, fused, monkeypatch):
     position; checked every 20 decode steps of a C1 real-time run."""
     from paper_2510_02758_b200 import dataplane as dpmod
 
-    seen = {"checked": 0, "bad": 0, "calls": 0}
+    seen = {"checked": 0, "bad": 0, "calls": 0, "recomputes": 0}
     orig = dpmod.GpuDataPlane.decode_done
+    orig_fill, orig_drop = dpmod.GpuDataPlane.fill_start, dpmod.GpuDataPlane.drop_host
     state = {}
+    stale = {}
 
     def decode_done(self, batch, made):
         orig(self, batch, made)
         seen["calls"] += 1
         if seen["calls"] % 20 == 0 and "eng" in state:
-            c, b = _host_mirror_mismatches(self, state["eng"], fused)
+            c, b = _host_mirror_mismatches(self, state["eng"], fused, stale)
             seen["checked"] += c
             seen["bad"] += b
+
+    def fill_start(self, job, eng):
+        if job.kind == "recompute":
+            seen["recomputes"] += 1
+            for rid in job.members:
+                stale[rid] = max(stale.get(rid, 0), eng.state[rid].kv.cpu_synced)
+        orig_fill(self, job, eng)
+
+    def drop_host(self, rid):
+        stale.pop(rid, None)
+        orig_drop(self, rid)
 
     from paper_2510_02758_b200.realtime import RealtimeEngine
 
@@ -184,6 +204,8 @@ def test_host_tier_bytes_equal_hbm_during_serving(cuda, fused, monkeypatch):
         state["eng"] = self
 
     monkeypatch.setattr(dpmod.GpuDataPlane, "decode_done", decode_done)
+    monkeypatch.setattr(dpmod.GpuDataPlane, "fill_start", fill_start)
+    monkeypatch.setattr(dpmod.GpuDataPlane, "drop_host", drop_host)
     monkeypatch.setattr(RealtimeEngine, "__init__", init)
     _run(cuda, engine=2, graphs=True, fused=fused)
     assert seen["checked"] > 1000, seen

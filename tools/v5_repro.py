@@ -49,7 +49,8 @@ def main():
     g = load_golden("runs", args.run)
     tr = load_trace(trace_path(g["trace"]))
     nb = pool_blocks(g["sim"], len(tr.requests))
-    pool = KvPool(nb, 8192, n_layers=2, kv_heads=2, head_dim=64, device=dev)
+    nh = g["sim"]["cpu_mem_tokens"] // 16 + len(tr.requests)
+    pool = KvPool(nb, nh, n_layers=2, kv_heads=2, head_dim=64, device=dev)
     dp = GpuDataPlane(tr.requests, pool, mode="replay", attention="all", n_q_heads=4)
     eng = Engine(tr, make_policy(g["policy"], SchedulerConfig(**g["sched"])), CostModel(**g["cm"]),
                  SimConfig(**g["sim"]), dataplane=dp)
