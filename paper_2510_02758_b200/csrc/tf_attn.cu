@@ -800,6 +800,36 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
       }
     }
   }
+  if (a.splits == 1 || !a.counters) return;
+  // ---- in-kernel split merge: the LAST split CTA of this (request, kv head)
+  // to arrive merges every split's partial (no separate combine launch, and
+  // nobody waits: the counter only elects the merger).  Writers publish with
+  // a fence before the counter increment; the merger reads through L2.
+  __shared__ int last_sh;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int prev = atomicAdd(a.counters + bh, 1);
+    last_sh = (prev == a.splits - 1);
+    if (last_sh) a.counters[bh] = 0;  // every split arrived: ready for the next launch
+  }
+  __syncthreads();
+  if (!last_sh) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
+    const int g = e / D, d = e % D;
+    const int64_t row = (int64_t)b * a.hq + kvh * G + g;
+    float mm = -FLT_MAX;
+    for (int sp = 0; sp < a.splits; ++sp) mm = fmaxf(mm, __ldcg(a.ws_ml + (row * a.splits + sp) * 2));
+    float ll = 0.f, aa = 0.f;
+    for (int sp = 0; sp < a.splits; ++sp) {
+      const float ms = __ldcg(a.ws_ml + (row * a.splits + sp) * 2);
+      const float f = ms == -FLT_MAX ? 0.f : exp2f(ms - mm);
+      ll += __ldcg(a.ws_ml + (row * a.splits + sp) * 2 + 1) * f;
+      aa += __ldcg(a.ws_acc + (row * a.splits + sp) * D + d) * f;
+    }
+    a.out[row * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(ll > 0.f ? aa / ll : 0.f));
+  }
 }
 
 
@@ -1209,6 +1239,13 @@ static void plan_splits(int B, int kv_heads, int max_ctx, int* splits, int* bps)
 
 static bool use_v4(int D, int G, int B) { return attn_impl() == 4 && D == 128 && G <= 8 && B <= kV4MaxB; }
 
+// v3 merges its splits in-kernel (last-arriving split CTA per (request, kv
+// head), counter region of FIXED size at the start of the workspace, for the
+// reason given at attn5_counter_bytes); other kernels use attn_combine_kernel
+constexpr int kV3MaxB = 4096;
+static bool v3_inkernel_merge(int D, int G, int B) { return attn_impl() >= 3 && attn_impl() != 4 && D == 128 && G <= 8 && B <= kV3MaxB; }
+static int64_t v3_counter_bytes(int kv) { return ((int64_t)kV3MaxB * kv * 4 + 255) / 256 * 256; }
+
 static int sm_count() {
   static int n = 0;
   if (!n) {
@@ -1271,7 +1308,7 @@ static int launch(const AttnArgs& a, int B, cudaStream_t st) {
     paged_attn_kernel<D, G><<<grid, kAttnWarps * 32, 0, st>>>(a);
   }
   TF_LAUNCH_CHECK();
-  if (a.splits > 1) {
+  if (a.splits > 1 && !a.counters) {
     attn_combine_kernel<D><<<B * a.hq, std::min(D, 128), 0, st>>>(a);
     TF_LAUNCH_CHECK();
   }
@@ -1297,7 +1334,8 @@ int64_t tf_paged_decode_attn_workspace(int64_t pool, int32_t B, int32_t max_ctx,
   int splits, bps;
   plan_splits(B, p->kv_heads, max_ctx, &splits, &bps);
   if (splits == 1) return 0;
-  return (int64_t)B * n_q_heads * splits * (p->head_dim + 2) * (int64_t)sizeof(float);
+  const int64_t cb = v3_inkernel_merge(p->head_dim, G, B) ? v3_counter_bytes(p->kv_heads) : 0;
+  return cb + (int64_t)B * n_q_heads * splits * (p->head_dim + 2) * (int64_t)sizeof(float);
 }
 
 int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, int32_t row_stride,
@@ -1360,12 +1398,13 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
   } else {
   plan_splits(B, p->kv_heads, max_ctx, &a.splits, &a.blocks_per_split);
   a.min_blocks_per_split = g_minblk;
-  int64_t need = a.splits == 1 ? 0 : (int64_t)B * n_q_heads * a.splits * (p->head_dim + 2) * (int64_t)sizeof(float);
+  const int64_t cb = (a.splits > 1 && v3_inkernel_merge(D, G, B)) ? v3_counter_bytes(p->kv_heads) : 0;
+  int64_t need = a.splits == 1 ? 0 : cb + (int64_t)B * n_q_heads * a.splits * (p->head_dim + 2) * (int64_t)sizeof(float);
   TF_CHECK_ARG(workspace_bytes >= need && (need == 0 || workspace), "tf_paged_decode_attn: workspace too small (%lld < %lld)",
                (long long)workspace_bytes, (long long)need);
-  a.ws_acc = (float*)workspace;
+  a.counters = cb ? (int32_t*)workspace : nullptr;
+  a.ws_acc = (float*)((char*)workspace + cb);
   a.ws_ml = a.ws_acc + (int64_t)B * n_q_heads * a.splits * p->head_dim;
-  a.counters = nullptr;
   a.kmax = 0;
   }
   cudaStream_t st = (cudaStream_t)stream;
