@@ -56,6 +56,7 @@ struct AttnArgs {
   int32_t B, kmax;
   int32_t* counters;
   int32_t mutate;  // test-only fault injection (attn_mutate)
+  int32_t balanced, ctas;  // v3: device-side balanced split plan over ~ctas CTAs (1-D grid)
 };
 
 // D = head_dim, G = q heads per kv head.
@@ -614,15 +615,73 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw) + warp * kWarpElems;
 
-  const int bh = blockIdx.y;
-  const int b = bh / a.kv_heads, kvh = bh % a.kv_heads;
-  const int split = blockIdx.x;
+  // ---- this CTA's (request b, kv head, split) and the split count of (b, kv head)
+  int b, kvh, split, nsplit, slot0;
+  if (a.balanced) {
+    // Device-side balanced plan (same on every CTA, from the contexts in HBM,
+    // so a captured graph re-plans for the batch it replays): every request
+    // is cut into ceil(nblk_b / per) splits with per = max(min, ceil(total
+    // blocks x kv / a.ctas)), so all CTAs carry ~the same number of blocks
+    // and the grid is ~a.ctas = a whole number of waves of resident CTAs - no
+    // wave tail, no dependence on a host-side max_ctx.  CTA i takes the i-th
+    // (b, kv head, split) in request-major order; CTAs past the last exit.
+    __shared__ int map_sh[5];
+    if (warp == 0) {
+      int tot = 0;
+      for (int base = 0; base < a.B; base += 32) {
+        const int bb = base + lane;
+        if (bb < a.B) tot += (__ldg(a.ctx + bb) + kBlk - 1) / kBlk;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      const int per = max(a.min_blocks_per_split, (tot * a.kv_heads + a.ctas - 1) / a.ctas);
+      const int me = blockIdx.x;
+      int carry = 0;
+      for (int base = 0; base < a.B; base += 32) {
+        const int bb = base + lane;
+        const int nb = bb < a.B ? (__ldg(a.ctx + bb) + kBlk - 1) / kBlk : 0;
+        const int sp = bb < a.B ? max(1, (nb + per - 1) / per) : 0;
+        const int v = sp * a.kv_heads;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const int excl = carry + incl - v;
+        if (bb < a.B && me >= excl && me < excl + v) {
+          map_sh[0] = bb;
+          map_sh[1] = (me - excl) / sp;
+          map_sh[2] = (me - excl) % sp;
+          map_sh[3] = sp;
+          map_sh[4] = excl + ((me - excl) / sp) * sp;
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0 && me >= carry) map_sh[0] = -1;
+    }
+    __syncthreads();
+    b = map_sh[0];
+    if (b < 0) return;  // uniform: the whole CTA has no work
+    kvh = map_sh[1];
+    split = map_sh[2];
+    nsplit = map_sh[3];
+    slot0 = map_sh[4];
+  } else {
+    b = blockIdx.y / a.kv_heads;
+    kvh = blockIdx.y % a.kv_heads;
+    split = blockIdx.x;
+    nsplit = a.splits;
+    slot0 = blockIdx.y * a.splits;
+  }
+  const int bh = b * a.kv_heads + kvh;
   const int ctx = a.ctx[b];
   const int nblk = (ctx + kBlk - 1) / kBlk;
   const int ctx_eff = (a.mutate == 1 && nblk >= 8) ? min(ctx, (nblk - nblk / 8) * kBlk) : ctx;
   // split size per request: a short request in a launch planned for a long
   // maximum context still spreads over all splits instead of idling them
-  const int bps = max(a.min_blocks_per_split, (nblk + a.splits - 1) / a.splits);
+  const int bps = a.balanced ? (nblk + nsplit - 1) / nsplit
+                             : max(a.min_blocks_per_split, (nblk + a.splits - 1) / a.splits);
   const int blk_lo = split * bps;
   const int blk_hi = min(nblk, blk_lo + bps);
   const int nmine = blk_hi > blk_lo + warp ? (blk_hi - blk_lo - warp + kV3Warps - 1) / kV3Warps : 0;
@@ -790,17 +849,19 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
       aa += acc_sh[(w * G + g) * D + d] * f;
     }
     const int64_t row = (int64_t)b * a.hq + kvh * G + g;
-    if (a.splits == 1) {
+    if (nsplit == 1) {
       a.out[row * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(ll > 0.f ? aa / ll : 0.f));
     } else {
-      a.ws_acc[(row * a.splits + split) * D + d] = aa;
+      // partial slot of (b, kv head, split): [slot][G][D] / [slot][G][2]
+      const int64_t pi = (int64_t)(slot0 + split) * G + g;
+      a.ws_acc[pi * D + d] = aa;
       if (d == 0) {
-        a.ws_ml[(row * a.splits + split) * 2 + 0] = mm;
-        a.ws_ml[(row * a.splits + split) * 2 + 1] = ll;
+        a.ws_ml[pi * 2 + 0] = mm;
+        a.ws_ml[pi * 2 + 1] = ll;
       }
     }
   }
-  if (a.splits == 1 || !a.counters) return;
+  if (nsplit == 1) return;
   // ---- in-kernel split merge: the LAST split CTA of this (request, kv head)
   // to arrive merges every split's partial (no separate combine launch, and
   // nobody waits: the counter only elects the merger).  Writers publish with
@@ -810,7 +871,7 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
   if (threadIdx.x == 0) {
     __threadfence();
     const int prev = atomicAdd(a.counters + bh, 1);
-    last_sh = (prev == a.splits - 1);
+    last_sh = (prev == nsplit - 1);
     if (last_sh) a.counters[bh] = 0;  // every split arrived: ready for the next launch
   }
   __syncthreads();
@@ -820,13 +881,14 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
     const int g = e / D, d = e % D;
     const int64_t row = (int64_t)b * a.hq + kvh * G + g;
     float mm = -FLT_MAX;
-    for (int sp = 0; sp < a.splits; ++sp) mm = fmaxf(mm, __ldcg(a.ws_ml + (row * a.splits + sp) * 2));
+    for (int sp = 0; sp < nsplit; ++sp) mm = fmaxf(mm, __ldcg(a.ws_ml + ((int64_t)(slot0 + sp) * G + g) * 2));
     float ll = 0.f, aa = 0.f;
-    for (int sp = 0; sp < a.splits; ++sp) {
-      const float ms = __ldcg(a.ws_ml + (row * a.splits + sp) * 2);
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const int64_t pi = (int64_t)(slot0 + sp) * G + g;
+      const float ms = __ldcg(a.ws_ml + pi * 2);
       const float f = ms == -FLT_MAX ? 0.f : exp2f(ms - mm);
-      ll += __ldcg(a.ws_ml + (row * a.splits + sp) * 2 + 1) * f;
-      aa += __ldcg(a.ws_acc + (row * a.splits + sp) * D + d) * f;
+      ll += __ldcg(a.ws_ml + pi * 2 + 1) * f;
+      aa += __ldcg(a.ws_acc + pi * D + d) * f;
     }
     a.out[row * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(ll > 0.f ? aa / ll : 0.f));
   }
@@ -1243,8 +1305,7 @@ static bool use_v4(int D, int G, int B) { return attn_impl() == 4 && D == 128 &&
 // head), counter region of FIXED size at the start of the workspace, for the
 // reason given at attn5_counter_bytes); other kernels use attn_combine_kernel
 constexpr int kV3MaxB = 4096;
-static bool v3_inkernel_merge(int D, int G, int B) { return attn_impl() >= 3 && attn_impl() != 4 && D == 128 && G <= 8 && B <= kV3MaxB; }
-static int64_t v3_counter_bytes(int kv) { return ((int64_t)kV3MaxB * kv * 4 + 255) / 256 * 256; }
+
 
 static int sm_count() {
   static int n = 0;
@@ -1255,6 +1316,36 @@ static int sm_count() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+static bool v3_used(int D, int G, int B) {
+  return attn_impl() >= 3 && attn_impl() != 4 && D == 128 && G <= 8 && B <= kV3MaxB;
+}
+static int64_t v3_counter_bytes(int kv) { return ((int64_t)kV3MaxB * kv * 4 + 255) / 256 * 256; }
+// v3 split plan: device-side balanced (default; TF_ATTN_BALANCED=0 for the
+// host plan_splits grid) over TF_ATTN_BWAVES waves of resident CTAs
+static int v3_balanced() {
+  static int b = -1;
+  if (b < 0) {
+    const char* e = getenv("TF_ATTN_BALANCED");
+    b = (e && e[0] == '0') ? 0 : 1;
+  }
+  return b;
+}
+static int v3_bwaves() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("TF_ATTN_BWAVES");
+    w = e ? std::max(1, atoi(e)) : 2;
+  }
+  return w;
+}
+static int v3_per_sm() { return v3_stages() == 2 ? 3 : 2; }
+static int v3_ctas() { return sm_count() * v3_per_sm() * v3_bwaves(); }
+// partial slots of a v3 launch (0: no split can happen)
+static int64_t v3_slots(int B, int kv, int splits) {
+  if (v3_balanced()) return (int64_t)v3_ctas() + (int64_t)B * kv;
+  return splits > 1 ? (int64_t)B * kv * splits : 0;
 }
 
 static int64_t v4_kmax(int max_ctx) { return (std::max(1, (max_ctx + kBlk - 1) / kBlk) + kPerMin - 1) / kPerMin + 1; }
@@ -1280,7 +1371,8 @@ static int launch(const AttnArgs& a, int B, cudaStream_t st) {
     return TF_OK;
   }
   dim3 grid(a.splits, B * a.kv_heads);
-  if (attn_impl() >= 3 && D == 128 && G <= 8) {
+  if (v3_used(D, G, B)) {
+    if (a.balanced) grid = dim3(a.ctas + B * a.kv_heads);
     constexpr int GG = G <= 8 ? G : 8;
     const int S = v3_stages();
     const int smem = kV3Warps * S * 2 * kBlk * kRowPad * 2;
@@ -1308,7 +1400,7 @@ static int launch(const AttnArgs& a, int B, cudaStream_t st) {
     paged_attn_kernel<D, G><<<grid, kAttnWarps * 32, 0, st>>>(a);
   }
   TF_LAUNCH_CHECK();
-  if (a.splits > 1 && !a.counters) {
+  if (!v3_used(D, G, B) && a.splits > 1) {
     attn_combine_kernel<D><<<B * a.hq, std::min(D, 128), 0, st>>>(a);
     TF_LAUNCH_CHECK();
   }
@@ -1333,9 +1425,12 @@ int64_t tf_paged_decode_attn_workspace(int64_t pool, int32_t B, int32_t max_ctx,
            (int64_t)B * p->kv_heads * v4_kmax(max_ctx) * G * (p->head_dim + 2) * (int64_t)sizeof(float);
   int splits, bps;
   plan_splits(B, p->kv_heads, max_ctx, &splits, &bps);
+  if (v3_used(p->head_dim, G, B)) {
+    const int64_t slots = v3_slots(B, p->kv_heads, splits);
+    return slots ? v3_counter_bytes(p->kv_heads) + slots * G * (p->head_dim + 2) * (int64_t)sizeof(float) : 0;
+  }
   if (splits == 1) return 0;
-  const int64_t cb = v3_inkernel_merge(p->head_dim, G, B) ? v3_counter_bytes(p->kv_heads) : 0;
-  return cb + (int64_t)B * n_q_heads * splits * (p->head_dim + 2) * (int64_t)sizeof(float);
+  return (int64_t)B * n_q_heads * splits * (p->head_dim + 2) * (int64_t)sizeof(float);
 }
 
 int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, int32_t row_stride,
@@ -1350,7 +1445,7 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
   TF_CHECK_ARG(B >= 0 && max_ctx >= 0, "tf_paged_decode_attn: bad B/max_ctx");
   if (B == 0) return TF_OK;
   TF_CHECK_ARG(q && dev_table && dev_rows && dev_ctx && out, "tf_paged_decode_attn: NULL pointer");
-  AttnArgs a;
+  AttnArgs a{};
   a.pool = p->gpu;
   a.q = (const uint16_t*)q;
   a.table = dev_table;
@@ -1398,14 +1493,29 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
   } else {
   plan_splits(B, p->kv_heads, max_ctx, &a.splits, &a.blocks_per_split);
   a.min_blocks_per_split = g_minblk;
-  const int64_t cb = (a.splits > 1 && v3_inkernel_merge(D, G, B)) ? v3_counter_bytes(p->kv_heads) : 0;
-  int64_t need = a.splits == 1 ? 0 : cb + (int64_t)B * n_q_heads * a.splits * (p->head_dim + 2) * (int64_t)sizeof(float);
-  TF_CHECK_ARG(workspace_bytes >= need && (need == 0 || workspace), "tf_paged_decode_attn: workspace too small (%lld < %lld)",
-               (long long)workspace_bytes, (long long)need);
-  a.counters = cb ? (int32_t*)workspace : nullptr;
-  a.ws_acc = (float*)((char*)workspace + cb);
-  a.ws_ml = a.ws_acc + (int64_t)B * n_q_heads * a.splits * p->head_dim;
   a.kmax = 0;
+  if (v3_used(D, G, B)) {
+    // v3: splits merged in-kernel; partials in [slot][G][D] / [slot][G][2]
+    a.balanced = v3_balanced();
+    a.ctas = a.balanced ? v3_ctas() : 0;
+    const int64_t slots = v3_slots(B, p->kv_heads, a.splits);
+    const int64_t cb = slots ? v3_counter_bytes(p->kv_heads) : 0;
+    const int64_t need = slots ? cb + slots * G * (D + 2) * (int64_t)sizeof(float) : 0;
+    TF_CHECK_ARG(workspace_bytes >= need && (need == 0 || workspace),
+                 "tf_paged_decode_attn: workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                 (long long)need);
+    a.counters = slots ? (int32_t*)workspace : nullptr;
+    a.ws_acc = (float*)((char*)workspace + cb);
+    a.ws_ml = a.ws_acc + slots * G * D;
+  } else {
+    int64_t need = a.splits == 1 ? 0 : (int64_t)B * n_q_heads * a.splits * (p->head_dim + 2) * (int64_t)sizeof(float);
+    TF_CHECK_ARG(workspace_bytes >= need && (need == 0 || workspace),
+                 "tf_paged_decode_attn: workspace too small (%lld < %lld)", (long long)workspace_bytes,
+                 (long long)need);
+    a.counters = nullptr;
+    a.ws_acc = (float*)workspace;
+    a.ws_ml = a.ws_acc + (int64_t)B * n_q_heads * a.splits * p->head_dim;
+  }
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (D == 128 && G == 4) return launch<128, 4>(a, B, st);
