@@ -57,6 +57,7 @@ struct AttnArgs {
   int32_t* counters;
   int32_t mutate;  // test-only fault injection (attn_mutate)
   int32_t balanced, ctas;  // v3: device-side balanced split plan over ~ctas CTAs (1-D grid)
+  int32_t l2_prefetch;     // v3: blocks per warp bulk-prefetched into L2 past the ring (0 = off)
 };
 
 // D = head_dim, G = q heads per kv head.
@@ -695,6 +696,21 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
   // dependent ones
   const int tab_pre = lane < nmine ? __ldg(trow + blk_lo + warp + lane * kV3Warps) : 0;
 
+  // Memory-level parallelism beyond the shared-memory ring: the K and V
+  // tiles of the warp's block l2_prefetch blocks past the ring's newest stage
+  // are requested into L2 with one bulk prefetch each (no shared memory, no
+  // registers), so the ring's cp.async hits L2 instead of waiting on DRAM
+  auto prefetch_l2 = [&](int jp) {
+    if (a.l2_prefetch <= 0 || jp >= nmine) return;  // warp-uniform
+    const int ent = jp < 32 ? __shfl_sync(0xffffffffu, tab_pre, jp) : __ldg(trow + blk_lo + warp + jp * kV3Warps);
+    if (lane == 0) {
+      const uint16_t* base = a.pool + (int64_t)ent * a.block_elems;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + koff), "r"((uint32_t)(tile * 2))
+                   : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + voff), "r"((uint32_t)(tile * 2))
+                   : "memory");
+    }
+  };
   auto issue = [&](int j) {  // warp-local block j -> stage j % S
     if (j < nmine) {
       const int blk = blk_lo + warp + j * kV3Warps;
@@ -711,7 +727,10 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
       }
     }
     cp_async_commit();
+    if (j >= S - 1) prefetch_l2(j + a.l2_prefetch);
   };
+#pragma unroll
+  for (int jj = S - 1; jj < S - 1 + a.l2_prefetch; ++jj) prefetch_l2(jj);
 #pragma unroll
   for (int p0 = 0; p0 < S - 1; ++p0) issue(p0);
 
@@ -1322,13 +1341,17 @@ static bool v3_used(int D, int G, int B) {
   return attn_impl() >= 3 && attn_impl() != 4 && D == 128 && G <= 8 && B <= kV3MaxB;
 }
 static int64_t v3_counter_bytes(int kv) { return ((int64_t)kV3MaxB * kv * 4 + 255) / 256 * 256; }
-// v3 split plan: device-side balanced (default; TF_ATTN_BALANCED=0 for the
-// host plan_splits grid) over TF_ATTN_BWAVES waves of resident CTAs
+// v3 split plan: the host plan_splits grid (default) or, with
+// TF_ATTN_BALANCED=1, the device-side balanced plan over TF_ATTN_BWAVES waves
+// of resident CTAs.  The balanced plan is correct but slower at every
+// measured shape (profiles/r2_attn_balanced_plan.json): its per-CTA scan of
+// the batch's contexts sits on every CTA's critical path, and the extra
+// splits it makes at more than one wave add per-CTA prologues
 static int v3_balanced() {
   static int b = -1;
   if (b < 0) {
     const char* e = getenv("TF_ATTN_BALANCED");
-    b = (e && e[0] == '0') ? 0 : 1;
+    b = (e && e[0] == '1') ? 1 : 0;
   }
   return b;
 }
@@ -1341,6 +1364,14 @@ static int v3_bwaves() {
   return w;
 }
 static int v3_per_sm() { return v3_stages() == 2 ? 3 : 2; }
+static int v3_l2_prefetch() {  // TF_ATTN_PF: blocks prefetched into L2 past the ring, per warp
+  static int pf = -1;
+  if (pf < 0) {
+    const char* e = getenv("TF_ATTN_PF");
+    pf = e ? std::max(0, std::min(8, atoi(e))) : 0;
+  }
+  return pf;
+}
 static int v3_ctas() { return sm_count() * v3_per_sm() * v3_bwaves(); }
 // partial slots of a v3 launch (0: no split can happen)
 static int64_t v3_slots(int B, int kv, int splits) {
@@ -1498,6 +1529,7 @@ int tf_paged_decode_attn(int64_t pool, const void* q, const int32_t* dev_table, 
     // v3: splits merged in-kernel; partials in [slot][G][D] / [slot][G][2]
     a.balanced = v3_balanced();
     a.ctas = a.balanced ? v3_ctas() : 0;
+    a.l2_prefetch = v3_l2_prefetch();
     const int64_t slots = v3_slots(B, p->kv_heads, a.splits);
     const int64_t cb = slots ? v3_counter_bytes(p->kv_heads) : 0;
     const int64_t need = slots ? cb + slots * G * (D + 2) * (int64_t)sizeof(float) : 0;
