@@ -113,6 +113,11 @@ int tf_copy_small(void* dst, const void* src, int64_t bytes, void* stream);
  * 8192), and y = silu(gu[:, :ffn]) * gu[:, ffn:] for gu [rows][2*ffn]. */
 int tf_rmsnorm(const void* x, const void* w, void* y, int32_t rows, int32_t dim, float eps, void* stream);
 int tf_silu_mul(const void* gu, void* y, int32_t rows, int32_t ffn, void* stream);
+/* x[r] = bf16(x[r] + y[r]) (in place), h[r] = rmsnorm(x[r]) * w; rows x dim bf16,
+ * dim % 8 == 0, dim <= 8192.  The TP=1 decoder's residual + next-norm after
+ * its output projections (plain GEMMs into y). */
+int tf_residual_rmsnorm(void* x, const void* y, const void* w, void* h, int32_t rows, int32_t dim, float eps,
+                        void* stream);
 
 /* ---------------------------------------------------------------- KV append --
  * Model path: write K/V rows of n tokens for one layer, token i at

@@ -122,6 +122,7 @@ SIGNATURES = {
     "tf_launch_floor": (C.c_int, [_P]),
     "tf_rmsnorm": (C.c_int, [_P, _P, _P, _I32, _I32, C.c_float, _P]),
     "tf_silu_mul": (C.c_int, [_P, _P, _I32, _I32, _P]),
+    "tf_residual_rmsnorm": (C.c_int, [_P, _P, _P, _P, _I32, _I32, C.c_float, _P]),
     "tf_kv_append": (C.c_int, [_I64, _P, _I32, _P, _P, _I32, _I32, _P, _P, _I64, _P]),
     "tf_rope_kv_append": (C.c_int, [_I64, _P, _I32, _P, _P, _I32, _I32, _P, _I32, _P, _P, _P, _P]),
     "tf_rope_kv_append_wt": (C.c_int, [_I64, _P, _P, _I32, _P, _P, _I32, _I32, _P, _I32, _P, _P, _P, _P]),

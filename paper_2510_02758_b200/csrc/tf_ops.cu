@@ -6,6 +6,8 @@
 //   tf_rmsnorm     y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w   (one CTA per row,
 //                  16-B vector loads, fp32 sum, row held in registers)
 //   tf_silu_mul    y = silu(gu[:, :F]) * gu[:, F:]                (one pass, 16-B vectors)
+//   tf_residual_rmsnorm  x += y; h = rmsnorm(x) * w                (residual add taken out of
+//                  the output-projection GEMM's epilogue, fused with the next norm)
 #include <algorithm>
 
 #include "tf_common.cuh"
@@ -82,6 +84,68 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* _
   }
 }
 
+// x[r] <- bf16(x[r] + y[r]); h[r] <- rmsnorm(x[r]) * w  (one CTA per row).  The
+// decode step's output projections (o_proj, down_proj) run as plain GEMMs
+// into y - 2 us faster per call than cuBLAS addmm with the residual in its
+// epilogue at the C2 shapes (profiles/r2_gemm_probe.json) - and this kernel
+// takes over the residual add from the epilogue together with the next
+// sub-layer's RMSNorm (same arithmetic as rmsnorm_kernel on the new x).
+__global__ void __launch_bounds__(kNormThreads) residual_rmsnorm_kernel(uint16_t* __restrict__ x,
+                                                                        const uint16_t* __restrict__ y,
+                                                                        const uint16_t* __restrict__ w,
+                                                                        uint16_t* __restrict__ h, int D, float eps) {
+  const int64_t row = blockIdx.x;
+  uint4* xr = reinterpret_cast<uint4*>(x + row * D);
+  const uint4* yr = reinterpret_cast<const uint4*>(y + row * D);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4* hr = reinterpret_cast<uint4*>(h + row * D);
+  const int nv = D / 8;
+  float v[kNormMaxVec][8];
+  uint4 gw[kNormMaxVec];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kNormMaxVec; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < nv) gw[k] = __ldg(wr + i);
+  }
+#pragma unroll
+  for (int k = 0; k < kNormMaxVec; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < nv) {
+      float a[8], b[8];
+      unpack8(yr[i], a);
+      unpack8(xr[i], b);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] += b[e];
+      const uint4 packed = pack8(a);  // the new residual is a bf16 tensor: round once
+      xr[i] = packed;
+      unpack8(packed, v[k]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += v[k][e] * v[k][e];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  __shared__ float part[kNormThreads / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < kNormThreads / 32; ++i) tot += part[i];
+  const float r = rsqrtf(tot / (float)D + eps);
+#pragma unroll
+  for (int k = 0; k < kNormMaxVec; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < nv) {
+      float g[8], o[8];
+      unpack8(gw[k], g);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(v[k][e] * r)) * g[e];
+      hr[i] = pack8(o);
+    }
+  }
+}
+
 // blockIdx.y = row, threads stride the row's 16-B vectors (no 64-bit division)
 __global__ void silu_mul_kernel(const uint16_t* __restrict__ gu, uint16_t* __restrict__ y, int64_t rows, int F) {
   const int nvr = F / 8;  // vectors per output row
@@ -116,6 +180,18 @@ int tf_rmsnorm(const void* x, const void* w, void* y, int32_t rows, int32_t dim,
   TF_CHECK_ARG(x && w && y, "tf_rmsnorm: NULL pointer");
   rmsnorm_kernel<<<rows, kNormThreads, 0, (cudaStream_t)stream>>>((const uint16_t*)x, (const uint16_t*)w,
                                                                   (uint16_t*)y, dim, eps);
+  TF_LAUNCH_CHECK();
+  return TF_OK;
+}
+
+int tf_residual_rmsnorm(void* x, const void* y, const void* w, void* h, int32_t rows, int32_t dim, float eps,
+                        void* stream) {
+  TF_CHECK_ARG(rows >= 0 && dim > 0 && dim % 8 == 0 && dim <= kNormThreads * kNormMaxVec * 8,
+               "tf_residual_rmsnorm: bad shape %d x %d", rows, dim);
+  if (rows == 0) return TF_OK;
+  TF_CHECK_ARG(x && y && w && h, "tf_residual_rmsnorm: NULL pointer");
+  residual_rmsnorm_kernel<<<rows, kNormThreads, 0, (cudaStream_t)stream>>>((uint16_t*)x, (const uint16_t*)y,
+                                                                           (const uint16_t*)w, (uint16_t*)h, dim, eps);
   TF_LAUNCH_CHECK();
   return TF_OK;
 }

@@ -184,6 +184,16 @@ class PagedDecoder:
         (tf_ar_residual_rmsnorm) does the all-reduce over NVLink, the residual
         add and the norm; otherwise addmm (+ NCCL all-reduce) and tf_rmsnorm."""
         ar = getattr(self.tp, "ar", None) if self.tp is not None and self.tp.size > 1 else None
+        if self.tp is None or self.tp.size == 1:
+            # plain GEMM (faster than addmm with the residual in the epilogue at
+            # decode shapes) + one fused residual-add / RMSNorm kernel
+            y = a @ w
+            h = torch.empty_like(x)
+            check(lib.tf_residual_rmsnorm(C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                          C.c_void_p(gamma.data_ptr()), C.c_void_p(h.data_ptr()), x.shape[0],
+                                          x.shape[1], self.s.rms_eps,
+                                          C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tf_residual_rmsnorm")
+            return x, h
         if ar is None or not ar.fits(x.shape[0], x.shape[1]):
             x = self._proj_residual(x, a, w)
             return x, self._rms(x, gamma)

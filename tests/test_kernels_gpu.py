@@ -226,6 +226,26 @@ def test_rmsnorm_vs_torch(cuda, rows, dim):
     assert ((y.float() - ref).abs() <= 2 ** -6 * ref.abs() + 1e-3).all()
 
 
+@pytest.mark.parametrize("rows,dim", [(1, 256), (64, 4096), (128, 5120), (300, 8192)])
+def test_residual_rmsnorm_bit_exact(cuda, rows, dim):
+    """x += y (one bf16 rounding of the fp32 sum), h = rmsnorm(x) * w: the new
+    residual equals the fp32 definition bit for bit and h equals tf_rmsnorm of it."""
+    lib = _lib()
+    x = (torch.randn(rows, dim, device=cuda) * 3).to(torch.bfloat16)
+    y = torch.randn(rows, dim, device=cuda).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(dim, device=cuda)).to(torch.bfloat16)
+    x_ref = (x.float() + y.float()).to(torch.bfloat16)
+    h = torch.empty_like(x)
+    lib.check(lib.lib.tf_residual_rmsnorm(C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                          C.c_void_p(w.data_ptr()), C.c_void_p(h.data_ptr()), rows, dim, 1e-5, None))
+    h_ref = torch.empty_like(x)
+    lib.check(lib.lib.tf_rmsnorm(C.c_void_p(x_ref.data_ptr()), C.c_void_p(w.data_ptr()),
+                                 C.c_void_p(h_ref.data_ptr()), rows, dim, 1e-5, None))
+    torch.cuda.synchronize()
+    assert torch.equal(x.view(torch.int16), x_ref.view(torch.int16))
+    assert torch.equal(h.view(torch.int16), h_ref.view(torch.int16))
+
+
 @pytest.mark.parametrize("rows,ffn", [(1, 688), (64, 14336), (200, 3456), (70000, 16)])
 def test_silu_mul_vs_torch(cuda, rows, ffn):
     import torch.nn.functional as F

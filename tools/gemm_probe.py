@@ -27,10 +27,11 @@ def time_graph(fn, reps=200):
             fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    for _ in range(reps // 10):
-        g.replay()
-    e1.record(s)
+    with torch.cuda.stream(s):  # replay on the stream the events are recorded on
+        e0.record(s)
+        for _ in range(reps // 10):
+            g.replay()
+        e1.record(s)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps * 1e3  # us
 
