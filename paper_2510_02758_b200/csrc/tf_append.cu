@@ -32,55 +32,67 @@ __global__ void append_kernel(PoolView pv, const int32_t* __restrict__ table, in
 
 // Fused decode epilogue of the QKV projection: rotary embedding of q and k
 // (interleaved pairs, angle = pos * inv_freq[i]) + append of k, v into the
-// paged pool + q written contiguously for the attention kernel.  One warp per
-// (token, head) of the fused [hq + 2*hkv] head axis.
-__global__ void rope_append_kernel(PoolView pv, const int32_t* __restrict__ table, int32_t stride,
-                                   const int32_t* __restrict__ rows, const int32_t* __restrict__ pos, int32_t n,
-                                   int32_t layer, const uint16_t* __restrict__ qkv, int32_t hq,
-                                   const float* __restrict__ inv_freq, uint16_t* __restrict__ q_out,
-                                   uint16_t* __restrict__ kv_out, const int32_t* __restrict__ host_table) {
-  const int heads = hq + 2 * pv.kv_heads;
-  const int warps = blockDim.x / 32;
-  const int64_t wid = (int64_t)blockIdx.x * warps + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (wid >= (int64_t)n * heads) return;
-  const int tok = (int)(wid / heads), h = (int)(wid % heads);
-  const int D = pv.head_dim;
-  const int p = pos[tok];
-  const uint16_t* src = qkv + ((int64_t)tok * heads + h) * D;
-  uint16_t* dst;
-  uint16_t* dst2 = nullptr;  // optional contiguous copy of the rotated k / v (prefill attention input)
-  uint16_t* dst3 = nullptr;  // optional host-store slot (fused write-through)
-  bool rotate = true;
-  if (h < hq) {
-    dst = q_out + ((int64_t)tok * hq + h) * D;
-  } else {
-    const int kvh = (h - hq) % pv.kv_heads, kv = (h - hq) / pv.kv_heads;
-    const int blk = table[(int64_t)rows[tok] * stride + p / pv.block_tokens];
-    dst = pv.gpu + pv.off(blk, layer, kv, kvh, p % pv.block_tokens);
-    rotate = (kv == 0);
-    if (kv_out) dst2 = kv_out + (((int64_t)kv * n + tok) * pv.kv_heads + kvh) * D;
-    if (host_table) {
-      // fused write-through: the same slot of the request's host block, written
-      // straight over PCIe into the mapped pinned store (posted writes)
-      const int hb = host_table[(int64_t)rows[tok] * stride + p / pv.block_tokens];
-      if (hb >= 0) dst3 = pv.host + pv.off(hb, layer, kv, kvh, p % pv.block_tokens);
-    }
+// paged pool + q written contiguously for the attention kernel (+ the
+// contiguous k / v copy a prefill's attention reads, + the host-store slot
+// when write-through is fused).  One CTA per token: the token's sin / cos
+// table (head_dim / 2 angles) is computed ONCE into shared memory and shared
+// by all its rotated heads (q and k), its pool / host block is looked up
+// once, and every head moves as 16-byte vectors (the earlier one-warp-per-
+// (token, head) version recomputed sincosf per head and moved 4-byte words).
+// The arithmetic per element is unchanged (bit-identical output).
+constexpr int kRopeThreads = 256;
+constexpr int kRopeMaxPairs = 128;  // head_dim <= 256
+
+__global__ void __launch_bounds__(kRopeThreads) rope_append_kernel(
+    PoolView pv, const int32_t* __restrict__ table, int32_t stride, const int32_t* __restrict__ rows,
+    const int32_t* __restrict__ pos, int32_t n, int32_t layer, const uint16_t* __restrict__ qkv, int32_t hq,
+    const float* __restrict__ inv_freq, uint16_t* __restrict__ q_out, uint16_t* __restrict__ kv_out,
+    const int32_t* __restrict__ host_table) {
+  __shared__ float sn_sh[kRopeMaxPairs], cs_sh[kRopeMaxPairs];
+  const int tok = blockIdx.x;
+  const int D = pv.head_dim, hkv = pv.kv_heads;
+  const int heads = hq + 2 * hkv;
+  const int p = __ldg(pos + tok);
+  const int row = __ldg(rows + tok);
+  const int lb = p / pv.block_tokens, slot = p % pv.block_tokens;
+  for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
+    float sn, cs;
+    sincosf((float)p * __ldg(inv_freq + i), &sn, &cs);
+    sn_sh[i] = sn;
+    cs_sh[i] = cs;
   }
-  for (int i = lane; i < D / 2; i += 32) {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 2 * i);
-    uint32_t o = w;
-    if (rotate) {
-      const float x1 = __uint_as_float(w << 16), x2 = __uint_as_float(w & 0xFFFF0000u);
-      float sn, cs;
-      sincosf((float)p * inv_freq[i], &sn, &cs);
-      const uint32_t o1 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * cs - x2 * sn));
-      const uint32_t o2 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * sn + x2 * cs));
-      o = o1 | (o2 << 16);
+  const int blk = __ldg(table + (int64_t)row * stride + lb);
+  const int hb = host_table ? __ldg(host_table + (int64_t)row * stride + lb) : -1;
+  __syncthreads();
+  const int vph = D / 8;  // 16-byte vectors per head
+  const uint4* src = reinterpret_cast<const uint4*>(qkv + (int64_t)tok * heads * D);
+  for (int v = threadIdx.x; v < heads * vph; v += blockDim.x) {
+    const int h = v / vph, d = (v - h * vph) * 8;
+    uint4 w = __ldg(src + v);
+    const bool is_q = h < hq;
+    const int kv = is_q ? 0 : (h - hq) / hkv, kvh = is_q ? 0 : (h - hq) % hkv;
+    if (is_q || kv == 0) {
+      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = d / 2 + k;
+        const float x1 = __uint_as_float(ws[k] << 16), x2 = __uint_as_float(ws[k] & 0xFFFF0000u);
+        const float sn = sn_sh[i], cs = cs_sh[i];
+        const uint32_t o1 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * cs - x2 * sn));
+        const uint32_t o2 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * sn + x2 * cs));
+        ws[k] = o1 | (o2 << 16);
+      }
+      w = make_uint4(ws[0], ws[1], ws[2], ws[3]);
     }
-    *reinterpret_cast<uint32_t*>(dst + 2 * i) = o;
-    if (dst2) *reinterpret_cast<uint32_t*>(dst2 + 2 * i) = o;
-    if (dst3) *reinterpret_cast<uint32_t*>(dst3 + 2 * i) = o;
+    if (is_q) {
+      *reinterpret_cast<uint4*>(q_out + ((int64_t)tok * hq + h) * D + d) = w;
+      continue;
+    }
+    *reinterpret_cast<uint4*>(pv.gpu + pv.off(blk, layer, kv, kvh, slot) + d) = w;
+    if (kv_out) *reinterpret_cast<uint4*>(kv_out + (((int64_t)kv * n + tok) * hkv + kvh) * D + d) = w;
+    // fused write-through: the same slot of the request's host block, written
+    // straight over PCIe into the mapped pinned store (posted writes)
+    if (hb >= 0) *reinterpret_cast<uint4*>(pv.host + pv.off(hb, layer, kv, kvh, slot) + d) = w;
   }
 }
 
@@ -183,8 +195,9 @@ int tf_rope_kv_append(int64_t pool, const int32_t* dev_table, int32_t row_stride
   TF_CHECK_ARG(n >= 0, "tf_rope_kv_append: n < 0");
   if (n == 0) return TF_OK;
   TF_CHECK_ARG(dev_table && dev_rows && dev_pos && qkv && inv_freq && q_out, "tf_rope_kv_append: NULL pointer");
-  const int64_t warps = (int64_t)n * (n_q_heads + 2 * p->kv_heads);
-  rope_append_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  TF_CHECK_ARG(p->head_dim % 8 == 0 && p->head_dim / 2 <= kRopeMaxPairs, "tf_rope_kv_append: head_dim %d",
+               p->head_dim);
+  rope_append_kernel<<<(unsigned)n, kRopeThreads, 0, (cudaStream_t)stream>>>(
       view_of(*p), dev_table, row_stride, dev_rows, dev_pos, n, layer, (const uint16_t*)qkv, n_q_heads, inv_freq,
       (uint16_t*)q_out, (uint16_t*)kv_out, nullptr);
   TF_LAUNCH_CHECK();
@@ -202,8 +215,9 @@ int tf_rope_kv_append_wt(int64_t pool, const int32_t* dev_table, const int32_t* 
   if (n == 0) return TF_OK;
   TF_CHECK_ARG(dev_table && dev_host_table && dev_rows && dev_pos && qkv && inv_freq && q_out,
                "tf_rope_kv_append_wt: NULL pointer");
-  const int64_t warps = (int64_t)n * (n_q_heads + 2 * p->kv_heads);
-  rope_append_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  TF_CHECK_ARG(p->head_dim % 8 == 0 && p->head_dim / 2 <= kRopeMaxPairs, "tf_rope_kv_append_wt: head_dim %d",
+               p->head_dim);
+  rope_append_kernel<<<(unsigned)n, kRopeThreads, 0, (cudaStream_t)stream>>>(
       view_of(*p), dev_table, row_stride, dev_rows, dev_pos, n, layer, (const uint16_t*)qkv, n_q_heads, inv_freq,
       (uint16_t*)q_out, (uint16_t*)kv_out, dev_host_table);
   TF_LAUNCH_CHECK();

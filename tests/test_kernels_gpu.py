@@ -210,6 +210,68 @@ def test_kv_append_writes_slots(cuda):
     p.close()
 
 
+@pytest.mark.parametrize("hq,hkv,D,n,wt", [(32, 8, 128, 128, False), (40, 8, 128, 5, False), (4, 2, 64, 300, False),
+                                           (32, 8, 128, 7, True)])
+def test_rope_kv_append_vs_torch(cuda, hq, hkv, D, n, wt):
+    """Fused rotary + paged append: q rotated into q_out, k rotated and v copied
+    into each token's pool slot (and the contiguous kv_out copy; with fused
+    write-through also into the host block), against a torch fp32 rotary."""
+    lib = _lib()
+    L, layer = 3, 1
+    nb = n // 16 + 4
+    p = _pool(cuda, 2 * nb + 2, 2 * nb + 2, L, hkv, D)
+    rows = torch.tensor([i % 2 for i in range(n)], dtype=torch.int32, device=cuda)
+    posl = [i // 2 + 3 * (i % 2) for i in range(n)]
+    pos = torch.tensor(posl, dtype=torch.int32, device=cuda)
+    nlb = max(posl) // 16 + 1
+    table = torch.tensor([list(range(nlb)), list(range(nb, nb + nlb))], dtype=torch.int32, device=cuda)
+    htable = torch.tensor([list(range(nlb, 2 * nlb)), list(range(0, nlb))], dtype=torch.int32, device=cuda)
+    heads = hq + 2 * hkv
+    qkv = torch.randn(n, heads, D, device=cuda).to(torch.bfloat16)
+    inv = 1.0 / (500000.0 ** (torch.arange(0, D, 2, device=cuda, dtype=torch.float32) / D))
+    q_out = torch.empty(n, hq, D, device=cuda, dtype=torch.bfloat16)
+    kv_out = torch.empty(2, n, hkv, D, device=cuda, dtype=torch.bfloat16)
+    if wt:
+        lib.check(lib.lib.tf_rope_kv_append_wt(p.handle, C.c_void_p(table.data_ptr()), C.c_void_p(htable.data_ptr()),
+                                               nlb, C.c_void_p(rows.data_ptr()), C.c_void_p(pos.data_ptr()), n, layer,
+                                               C.c_void_p(qkv.data_ptr()), hq, C.c_void_p(inv.data_ptr()),
+                                               C.c_void_p(q_out.data_ptr()), C.c_void_p(kv_out.data_ptr()), None))
+    else:
+        lib.check(lib.lib.tf_rope_kv_append(p.handle, C.c_void_p(table.data_ptr()), nlb, C.c_void_p(rows.data_ptr()),
+                                            C.c_void_p(pos.data_ptr()), n, layer, C.c_void_p(qkv.data_ptr()), hq,
+                                            C.c_void_p(inv.data_ptr()), C.c_void_p(q_out.data_ptr()),
+                                            C.c_void_p(kv_out.data_ptr()), None))
+    torch.cuda.synchronize()
+
+    def rope(x):  # interleaved pairs, fp32
+        ang = pos.float()[:, None, None] * inv[None, None, :]
+        x1, x2 = x[..., 0::2].float(), x[..., 1::2].float()
+        out = torch.empty_like(x, dtype=torch.float32)
+        out[..., 0::2] = x1 * ang.cos() - x2 * ang.sin()
+        out[..., 1::2] = x1 * ang.sin() + x2 * ang.cos()
+        return out
+
+    q_ref = rope(qkv[:, :hq])
+    k_ref = rope(qkv[:, hq:hq + hkv])
+    v_ref = qkv[:, hq + hkv:]
+    tol = lambda r: 2 ** -7 * r.abs() + 2 ** -12  # noqa: E731  (bf16 rounding + sincos ulps)
+    assert ((q_out.float() - q_ref).abs() <= tol(q_ref)).all()
+    assert ((kv_out[0].float() - k_ref).abs() <= tol(k_ref)).all()
+    assert torch.equal(kv_out[1], v_ref)
+    g = p.gpu_view().view(torch.bfloat16)
+    hv = p.host_view().view(torch.bfloat16)
+    for i in range(n):
+        r, ps = int(rows[i]), posl[i]
+        blk = int(table[r, ps // 16])
+        assert torch.equal(g[blk, layer, 0, :, ps % 16], kv_out[0, i])
+        assert torch.equal(g[blk, layer, 1, :, ps % 16], kv_out[1, i])
+        if wt:
+            hb = int(htable[r, ps // 16])
+            assert torch.equal(hv[hb, layer, 0, :, ps % 16], kv_out[0, i].cpu())
+            assert torch.equal(hv[hb, layer, 1, :, ps % 16], kv_out[1, i].cpu())
+    p.close()
+
+
 @pytest.mark.parametrize("rows,dim", [(1, 256), (37, 4096), (128, 5120), (3000, 4096)])
 def test_rmsnorm_vs_torch(cuda, rows, dim):
     import torch.nn.functional as F
