@@ -1,0 +1,114 @@
+"""The decode step end to end against a plain PyTorch fp32 reference.
+
+The paged decoder's decode forward (model.PagedDecoder._decode_rows: fused
+RMSNorm, QKV GEMM, fused rotary + paged append, paged decode attention,
+output GEMMs + fused residual/RMSNorm, SwiGLU) is compared with an fp32
+restatement that reads the SAME cached K/V out of the pool for the past
+positions and computes everything else from the weights: logits per row
+within 2e-2 of the row's max |logit| (the north star's bf16 tolerance), and
+the K/V the step appended equal to the reference's within bf16 rounding.
+Covers head_dim 64 (the C1 tiny decoder, bulk-copy attention) and head_dim
+128 (the tensor-core attention the C2 models use)."""
+import dataclasses
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _rms(x, w, eps):
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * w.float()
+
+
+def _rope(x, pos, inv):  # x [n, heads, hd] fp32, interleaved pairs
+    ang = pos.float()[:, None, None] * inv[None, None, :]
+    x1, x2 = x[..., 0::2], x[..., 1::2]
+    out = torch.empty_like(x)
+    out[..., 0::2] = x1 * ang.cos() - x2 * ang.sin()
+    out[..., 1::2] = x1 * ang.sin() + x2 * ang.cos()
+    return out
+
+
+def _reference_decode(model, dp, rids, toks, positions):
+    """fp32 decode step: past K/V from the pool (bf16 bits as cached), the new
+    token's K/V computed here.  Returns (logits [B, vocab], new k/v per layer)."""
+    s = model.s
+    hq, hkv, hd = model.hq, model.hkv, s.head_dim
+    G = hq // hkv
+    pv = dp.pool.gpu_view().view(torch.bfloat16)  # [blocks, L, 2, H, 16, D]
+    tab = dp.table
+    pos = torch.tensor(positions, device=model.device)
+    x = model.embed[toks].float()
+    new_kv = []
+    for li, L in enumerate(model.layers):
+        h = _rms(x, L["ln1"], s.rms_eps)
+        qkv = h @ L["wqkv"].float()
+        if "bqkv" in L:
+            qkv = qkv + L["bqkv"].float()
+        q = qkv[:, : hq * hd].view(-1, hq, hd)
+        k = qkv[:, hq * hd:(hq + hkv) * hd].view(-1, hkv, hd)
+        v = qkv[:, (hq + hkv) * hd:].view(-1, hkv, hd)
+        q, k = _rope(q, pos, model._inv_freq), _rope(k, pos, model._inv_freq)
+        new_kv.append((k, v))
+        outs = []
+        for b, (rid, p) in enumerate(zip(rids, positions)):
+            idx = torch.arange(p, device=model.device)
+            blocks = tab[rid, idx // 16].long()
+            kc = pv[blocks, li, 0, :, idx % 16].float()  # [p, H, D]
+            vc = pv[blocks, li, 1, :, idx % 16].float()
+            kk = torch.cat([kc, k[b][None]], 0)  # [p+1, H, D]
+            vv = torch.cat([vc, v[b][None]], 0)
+            kk, vv = kk.repeat_interleave(G, dim=1), vv.repeat_interleave(G, dim=1)
+            sc = torch.einsum("hd,thd->ht", q[b], kk) / math.sqrt(hd)
+            outs.append(torch.einsum("ht,thd->hd", sc.softmax(-1), vv).reshape(-1))
+        a = torch.stack(outs)
+        x = x + a @ L["wo"].float()
+        h2 = _rms(x, L["ln2"], s.rms_eps)
+        gu = h2 @ L["wgu"].float()
+        act = torch.nn.functional.silu(gu[:, : model.ffn]) * gu[:, model.ffn:]
+        x = x + act @ L["wd"].float()
+    return _rms(x, model.ln_f, s.rms_eps) @ model.lm_head.float(), new_kv
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_decode_step_matches_fp32_reference(cuda, hd):
+    from test_tp_gpu import _setup
+
+    from paper_2510_02758_b200 import configs
+
+    shape = configs.TINY if hd == 64 else dataclasses.replace(
+        configs.TINY, name="mini-hd128", hidden=512, n_q_heads=8, n_kv_heads=2, head_dim=128, ffn=1024)
+    n_req, nlb = 6, 8
+    g = torch.Generator().manual_seed(hd)
+    seqs = [(i, torch.randint(0, shape.vocab, (20 + 17 * i,), generator=g), 0) for i in range(n_req)]
+    model, dp, pool = _setup(cuda, shape, None, n_req, nlb)
+    # non-trivial norm weights (the synthetic model's are ones)
+    for L in model.layers:
+        L["ln1"].copy_((1 + 0.2 * torch.randn(shape.hidden, device=cuda)).to(torch.bfloat16))
+        L["ln2"].copy_((1 + 0.2 * torch.randn(shape.hidden, device=cuda)).to(torch.bfloat16))
+    st = dp.s_compute
+    with torch.cuda.stream(st):
+        first = model._prefill_batch(dp, seqs, st)
+    torch.cuda.synchronize()
+    rids = [0, 2, 3, 5, 1]  # a subset, out of order
+    positions = [seqs[r][1].numel() for r in rids]
+    toks = first[rids].to(torch.long)
+    ref_logits, ref_kv = _reference_decode(model, dp, rids, toks, positions)
+    model.keep_logits = True
+    with torch.cuda.stream(st):
+        model._decode_rows(dp, rids, toks, positions, st)
+    torch.cuda.synchronize()
+    lg = model.last_logits.float()
+    err = (lg - ref_logits).abs().amax(-1)
+    tol = 2e-2 * ref_logits.abs().amax(-1) + 2.0 ** -8
+    assert bool((err <= tol).all()), f"decode logits off by {err.tolist()} (tol {tol.tolist()})"
+    # the appended K / V slots: bf16 of the reference within a few bf16 ulps
+    pv = pool.gpu_view().view(torch.bfloat16)
+    for li, (k, v) in enumerate(ref_kv):
+        for b, (rid, p) in enumerate(zip(rids, positions)):
+            blk = int(dp.table[rid, p // 16])
+            gk, gv = pv[blk, li, 0, :, p % 16].float(), pv[blk, li, 1, :, p % 16].float()
+            assert ((gk - k[b]).abs() <= 2 ** -6 * k[b].abs() + 2 ** -8).all(), f"layer {li} row {b}: K"
+            assert ((gv - v[b]).abs() <= 2 ** -6 * v[b].abs() + 2 ** -8).all(), f"layer {li} row {b}: V"
