@@ -6,7 +6,8 @@ output GEMMs + fused residual/RMSNorm, SwiGLU) is compared with an fp32
 restatement that reads the SAME cached K/V out of the pool for the past
 positions and computes everything else from the weights: logits per row
 within 2e-2 of the row's max |logit| (the north star's bf16 tolerance), and
-the K/V the step appended equal to the reference's within bf16 rounding.
+the K/V the step appended within bf16 rounding of the reference at layer 0
+and within the same 2e-2 tolerance deeper (bf16 residual stream).
 Covers head_dim 64 (the C1 tiny decoder, bulk-copy attention) and head_dim
 128 (the tensor-core attention the C2 models use)."""
 import dataclasses
@@ -104,11 +105,15 @@ def test_decode_step_matches_fp32_reference(cuda, hd):
     err = (lg - ref_logits).abs().amax(-1)
     tol = 2e-2 * ref_logits.abs().amax(-1) + 2.0 ** -8
     assert bool((err <= tol).all()), f"decode logits off by {err.tolist()} (tol {tol.tolist()})"
-    # the appended K / V slots: bf16 of the reference within a few bf16 ulps
+    # the appended K / V slots against the reference
     pv = pool.gpu_view().view(torch.bfloat16)
     for li, (k, v) in enumerate(ref_kv):
         for b, (rid, p) in enumerate(zip(rids, positions)):
             blk = int(dp.table[rid, p // 16])
             gk, gv = pv[blk, li, 0, :, p % 16].float(), pv[blk, li, 1, :, p % 16].float()
-            assert ((gk - k[b]).abs() <= 2 ** -6 * k[b].abs() + 2 ** -8).all(), f"layer {li} row {b}: K"
-            assert ((gv - v[b]).abs() <= 2 ** -6 * v[b].abs() + 2 ** -8).all(), f"layer {li} row {b}: V"
+            # layer 0 sees the same inputs as the reference up to bf16 rounding of
+            # one GEMM; deeper layers inherit the bf16 residual stream, so they
+            # get the north-star tolerance (2e-2 of the row's magnitude)
+            for got, ref, what in ((gk, k[b], "K"), (gv, v[b], "V")):
+                tol = (2 ** -6 * ref.abs() + 2 ** -8) if li == 0 else (2e-2 * ref.abs().max() + 2 ** -8)
+                assert ((got - ref).abs() <= tol).all(), f"layer {li} row {b}: {what}"
