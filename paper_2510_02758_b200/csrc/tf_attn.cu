@@ -604,7 +604,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 // S = ring stages per warp (S - 1 blocks in flight); 2 stages fit 3 CTAs per
 // SM (12 warps), 3 stages 2 CTAs per SM (8 warps).
-template <int G, int S>
+__device__ __forceinline__ uint32_t movt3(uint32_t x) {  // transpose an 8x8 bf16 fragment across the warp
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+// TR = transposed contractions (v5's math inside v3's grid): S^T[16 tokens][8
+// heads] = K Q^T and O^T[D][8 heads] += V^T P^T - the G <= 8 q heads fill the
+// N = 8 side of m16n8k16 instead of G of the 16 M rows, so a block costs 16
+// MMAs instead of 32 and the output accumulators 32 registers instead of 64.
+template <int G, int S, bool TR>
 __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_kernel(const AttnArgs a) {
   constexpr int D = 128;
   static_assert(G >= 1 && G <= 8, "v3 packs the group into rows 0..7 of the 16-row tile");
@@ -734,124 +744,239 @@ __global__ void __launch_bounds__(kV3Warps * 32, S == 2 ? 3 : 2) paged_attn_mma_
 #pragma unroll
   for (int p0 = 0; p0 < S - 1; ++p0) issue(p0);
 
-  // Q as the A operand: rows 0..G-1 = the group's heads (scaled later), rest 0
+  // ---- per-warp partial in a uniform shape for the epilogue: head g of the
+  // group -> acc over D, running max, sum
   const int r0 = lane >> 2, cq = (lane & 3) * 2;
-  uint32_t qa[8][4];
-#pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    uint32_t lo = 0, hi = 0;
-    if (r0 < G) {
-      const uint16_t* qrow = a.q + ((int64_t)b * a.hq + kvh * G + r0) * D + kk * 16 + cq;
-      lo = *reinterpret_cast<const uint32_t*>(qrow);
-      hi = *reinterpret_cast<const uint32_t*>(qrow + 8);
-    }
-    qa[kk][0] = lo;
-    qa[kk][1] = 0;  // row r0 + 8 >= 8 > G - 1
-    qa[kk][2] = hi;
-    qa[kk][3] = 0;
-  }
-  float o[16][4];
+  float m_fin[2], l_fin[2];  // TR: heads h0, h0 + 1; v3: row r0 in [0]
+  float o[16][4];            // v3: [n-tile of 8 dims][c]; TR uses o[0..7] as [m-tile of 16 dims][c]
 #pragma unroll
   for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  float m0 = -FLT_MAX, l0 = 0.f;  // row r0 (rows r0+8 are padding)
-
-  for (int j = 0; j < nmine; ++j) {
-    issue(j + S - 1);
-    cp_async_wait<S - 1>();
-    __syncwarp();
-    const uint16_t* ks = ring + (j % S) * 2 * kTileElems;
-    const uint16_t* vs = ks + kTileElems;
-    const int blk = blk_lo + warp + j * kV3Warps;
-    // ---- S = Q K^T : two n-tiles of 8 tokens, 8 k-steps of 16 dims
-    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row within matrix, matrix id
+  if constexpr (TR) {
+    // B operand Q^T: head g4 = r0 (zero past G), dims 16kk + 2q4 (+1), (+8)
+    uint32_t qb[8][2];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      uint32_t b00, b01, b10, b11;
-      // matrices: (tok 0-7, dims lo), (tok 0-7, dims hi), (tok 8-15, dims lo), (tok 8-15, dims hi)
-      const uint16_t* p = ks + ((lm >> 1) * 8 + lr) * kRowPad + kk * 16 + (lm & 1) * 8;
-      ldsm_x4(b00, b01, b10, b11, p);
-      mma_bf16(s[0], qa[kk], b00, b01);
-      mma_bf16(s[1], qa[kk], b10, b11);
+      const uint16_t* qrow = a.q + ((int64_t)b * a.hq + kvh * G + (r0 < G ? r0 : 0)) * D + kk * 16 + cq;
+      qb[kk][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(qrow) : 0u;
+      qb[kk][1] = r0 < G ? *reinterpret_cast<const uint32_t*>(qrow + 8) : 0u;
     }
-    // ---- online softmax on row r0 (c0, c1 of each n-tile)
-    float mx = -FLT_MAX;
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int t = nt * 8 + cq + e;
-        float v = s[nt][e] * a.scale_log2;
-        if (blk * kBlk + t >= ctx_eff) v = -FLT_MAX;
-        s[nt][e] = v;
-        mx = fmaxf(mx, v);
-      }
-    }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float mn = fmaxf(m0, mx);
-    const float alpha = exp2f(m0 - mn);
-    m0 = mn;
-    float ps = 0.f;
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const float p = s[nt][e] > -FLT_MAX ? exp2f(s[nt][e] - mn) : 0.f;
-        s[nt][e] = p;
-        ps += p;
-      }
-    }
-    l0 = l0 * alpha + ps;
-#pragma unroll
-    for (int n = 0; n < 16; ++n) {
-      o[n][0] *= alpha;
-      o[n][1] *= alpha;
-    }
-    // ---- O += P V : P from the S accumulators (rows r0 / r0+8 = 0), V via ldmatrix.trans
-    uint32_t pa[4];
-    pa[0] = pack_bf16(s[0][0], s[0][1]);
-    pa[1] = 0;
-    pa[2] = pack_bf16(s[1][0], s[1][1]);
-    pa[3] = 0;
-    const int valid = ctx - blk * kBlk;
-    if (valid < kBlk) {
-      // V slots past ctx may hold stale bits (NaN * 0 = NaN in the MMA): zero them
-      uint16_t* vw = const_cast<uint16_t*>(vs);
-      for (int e = lane; e < (kBlk - valid) * (D / 8); e += 32) {
-        const int r = valid + e / (D / 8), c8 = e % (D / 8);
-        *reinterpret_cast<uint4*>(vw + r * kRowPad + c8 * 8) = make_uint4(0, 0, 0, 0);
-      }
+    float m_0 = -FLT_MAX, m_1 = -FLT_MAX, l_0 = 0.f, l_1 = 0.f;
+    const int lr = lane & 7, mi = lane >> 3;
+    const int k_row = (mi & 1) * 8 + lr, k_cadd = mi >> 1;  // K as the A operand (non-trans)
+    const int v_row = (mi >> 1) * 8 + lr, v_cadd = mi & 1;  // V^T as the A operand (.trans)
+    for (int j = 0; j < nmine; ++j) {
+      issue(j + S - 1);
+      cp_async_wait<S - 1>();
       __syncwarp();
-    }
+      const uint16_t* ks = ring + (j % S) * 2 * kTileElems;
+      const uint16_t* vs = ks + kTileElems;
+      const int blk = blk_lo + warp + j * kV3Warps;
+      // S^T = K Q^T, two accumulators (even / odd k-steps) halve the MMA chain
+      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int np = 0; np < 8; ++np) {  // pairs of 8-dim n-tiles
-      uint32_t v0, v1, v2, v3;
-      // matrices: (tok 0-7, dims 16np..+8), (tok 8-15, same), (tok 0-7, dims +8), (tok 8-15, dims +8)
-      const uint16_t* p = vs + ((lm & 1) * 8 + lr) * kRowPad + np * 16 + (lm >> 1) * 8;
-      ldsm_x4_t(v0, v1, v2, v3, p);
-      mma_bf16(o[2 * np], pa, v0, v1);
-      mma_bf16(o[2 * np + 1], pa, v2, v3);
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t a0_, a1_, a2_, a3_;
+        ldsm_x4(a0_, a1_, a2_, a3_, ks + k_row * kRowPad + kk * 16 + k_cadd * 8);
+        const uint32_t af[4] = {a0_, a1_, a2_, a3_};
+        mma_bf16((kk & 1) ? sb : sa, af, qb[kk][0], qb[kk][1]);
+      }
+      // online softmax per head (this thread: tokens r0, r0 + 8; heads cq, cq + 1)
+      const int t0 = blk * kBlk + r0;
+      float s00 = (sa[0] + sb[0]) * a.scale_log2, s01 = (sa[1] + sb[1]) * a.scale_log2;
+      float s10 = (sa[2] + sb[2]) * a.scale_log2, s11 = (sa[3] + sb[3]) * a.scale_log2;
+      if (t0 >= ctx_eff) s00 = s01 = -FLT_MAX;
+      if (t0 + 8 >= ctx_eff) s10 = s11 = -FLT_MAX;
+      float mx0 = fmaxf(s00, s10), mx1 = fmaxf(s01, s11);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float mn0 = fmaxf(m_0, mx0), mn1 = fmaxf(m_1, mx1);
+      const float al0 = exp2f(m_0 - mn0), al1 = exp2f(m_1 - mn1);
+      m_0 = mn0;
+      m_1 = mn1;
+      const float p00 = s00 > -FLT_MAX ? exp2f(s00 - mn0) : 0.f;
+      const float p01 = s01 > -FLT_MAX ? exp2f(s01 - mn1) : 0.f;
+      const float p10 = s10 > -FLT_MAX ? exp2f(s10 - mn0) : 0.f;
+      const float p11 = s11 > -FLT_MAX ? exp2f(s11 - mn1) : 0.f;
+      l_0 = l_0 * al0 + p00 + p10;
+      l_1 = l_1 * al1 + p01 + p11;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        o[mt][0] *= al0;
+        o[mt][1] *= al1;
+        o[mt][2] *= al0;
+        o[mt][3] *= al1;
+      }
+      // P^T (tokens x heads) -> B operand (tokens along the quad index)
+      const uint32_t pb0 = movt3(pack_bf16(p00, p01));
+      const uint32_t pb1 = movt3(pack_bf16(p10, p11));
+      const int valid = ctx - blk * kBlk;
+      if (valid < kBlk) {
+        // V slots past ctx may hold stale bits (NaN * 0 = NaN in the MMA): zero them
+        uint16_t* vw = const_cast<uint16_t*>(vs);
+        for (int e = lane; e < (kBlk - valid) * (D / 8); e += 32) {
+          const int r = valid + e / (D / 8), c8 = e % (D / 8);
+          *reinterpret_cast<uint4*>(vw + r * kRowPad + c8 * 8) = make_uint4(0, 0, 0, 0);
+        }
+        __syncwarp();
+      }
+      // O^T += V^T P^T: 8 m-tiles of 16 dims
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t a0_, a1_, a2_, a3_;
+        ldsm_x4_t(a0_, a1_, a2_, a3_, vs + v_row * kRowPad + mt * 16 + v_cadd * 8);
+        const uint32_t af[4] = {a0_, a1_, a2_, a3_};
+        mma_bf16(o[mt], af, pb0, pb1);
+      }
+      __syncwarp();  // the stage is refilled by issue(j + S - 1) next iteration
     }
-    __syncwarp();  // the stage is refilled by issue(j + 3) next iteration
+    cp_async_wait<0>();
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      l_0 += __shfl_xor_sync(0xffffffffu, l_0, off);
+      l_1 += __shfl_xor_sync(0xffffffffu, l_1, off);
+    }
+    m_fin[0] = m_0;
+    m_fin[1] = m_1;
+    l_fin[0] = l_0;
+    l_fin[1] = l_1;
+  } else {
+    // Q as the A operand: rows 0..G-1 = the group's heads (scaled later), rest 0
+    uint32_t qa[8][4];
+  #pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t lo = 0, hi = 0;
+      if (r0 < G) {
+        const uint16_t* qrow = a.q + ((int64_t)b * a.hq + kvh * G + r0) * D + kk * 16 + cq;
+        lo = *reinterpret_cast<const uint32_t*>(qrow);
+        hi = *reinterpret_cast<const uint32_t*>(qrow + 8);
+      }
+      qa[kk][0] = lo;
+      qa[kk][1] = 0;  // row r0 + 8 >= 8 > G - 1
+      qa[kk][2] = hi;
+      qa[kk][3] = 0;
+    }
+    float m0 = -FLT_MAX, l0 = 0.f;  // row r0 (rows r0+8 are padding)
+
+    for (int j = 0; j < nmine; ++j) {
+      issue(j + S - 1);
+      cp_async_wait<S - 1>();
+      __syncwarp();
+      const uint16_t* ks = ring + (j % S) * 2 * kTileElems;
+      const uint16_t* vs = ks + kTileElems;
+      const int blk = blk_lo + warp + j * kV3Warps;
+      // ---- S = Q K^T : two n-tiles of 8 tokens, 8 k-steps of 16 dims
+      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row within matrix, matrix id
+  #pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t b00, b01, b10, b11;
+        // matrices: (tok 0-7, dims lo), (tok 0-7, dims hi), (tok 8-15, dims lo), (tok 8-15, dims hi)
+        const uint16_t* p = ks + ((lm >> 1) * 8 + lr) * kRowPad + kk * 16 + (lm & 1) * 8;
+        ldsm_x4(b00, b01, b10, b11, p);
+        mma_bf16(s[0], qa[kk], b00, b01);
+        mma_bf16(s[1], qa[kk], b10, b11);
+      }
+      // ---- online softmax on row r0 (c0, c1 of each n-tile)
+      float mx = -FLT_MAX;
+  #pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+  #pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int t = nt * 8 + cq + e;
+          float v = s[nt][e] * a.scale_log2;
+          if (blk * kBlk + t >= ctx_eff) v = -FLT_MAX;
+          s[nt][e] = v;
+          mx = fmaxf(mx, v);
+        }
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float mn = fmaxf(m0, mx);
+      const float alpha = exp2f(m0 - mn);
+      m0 = mn;
+      float ps = 0.f;
+  #pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+  #pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float p = s[nt][e] > -FLT_MAX ? exp2f(s[nt][e] - mn) : 0.f;
+          s[nt][e] = p;
+          ps += p;
+        }
+      }
+      l0 = l0 * alpha + ps;
+  #pragma unroll
+      for (int n = 0; n < 16; ++n) {
+        o[n][0] *= alpha;
+        o[n][1] *= alpha;
+      }
+      // ---- O += P V : P from the S accumulators (rows r0 / r0+8 = 0), V via ldmatrix.trans
+      uint32_t pa[4];
+      pa[0] = pack_bf16(s[0][0], s[0][1]);
+      pa[1] = 0;
+      pa[2] = pack_bf16(s[1][0], s[1][1]);
+      pa[3] = 0;
+      const int valid = ctx - blk * kBlk;
+      if (valid < kBlk) {
+        // V slots past ctx may hold stale bits (NaN * 0 = NaN in the MMA): zero them
+        uint16_t* vw = const_cast<uint16_t*>(vs);
+        for (int e = lane; e < (kBlk - valid) * (D / 8); e += 32) {
+          const int r = valid + e / (D / 8), c8 = e % (D / 8);
+          *reinterpret_cast<uint4*>(vw + r * kRowPad + c8 * 8) = make_uint4(0, 0, 0, 0);
+        }
+        __syncwarp();
+      }
+  #pragma unroll
+      for (int np = 0; np < 8; ++np) {  // pairs of 8-dim n-tiles
+        uint32_t v0, v1, v2, v3;
+        // matrices: (tok 0-7, dims 16np..+8), (tok 8-15, same), (tok 0-7, dims +8), (tok 8-15, dims +8)
+        const uint16_t* p = vs + ((lm & 1) * 8 + lr) * kRowPad + np * 16 + (lm >> 1) * 8;
+        ldsm_x4_t(v0, v1, v2, v3, p);
+        mma_bf16(o[2 * np], pa, v0, v1);
+        mma_bf16(o[2 * np + 1], pa, v2, v3);
+      }
+      __syncwarp();  // the stage is refilled by issue(j + 3) next iteration
+    }
+    cp_async_wait<0>();
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    m_fin[0] = m0;
+    l_fin[0] = l0;
   }
-  cp_async_wait<0>();
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
 
   // ---- merge the 4 warps (reuse the ring memory), write split / output
   __syncthreads();
   float* acc_sh = reinterpret_cast<float*>(smem_raw);  // [kV3Warps][G][D]
   __shared__ float m_sh[kV3Warps][8], l_sh[kV3Warps][8];
-  if (r0 < G) {
+  if constexpr (TR) {
+    // o[mt][0 / 2]: head cq at dims 16mt + r0 (+ 8); o[mt][1 / 3]: head cq + 1
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int h = cq + hh;
+      if (h < G) {
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          acc_sh[(warp * G + h) * D + 16 * mt + r0] = o[mt][hh];
+          acc_sh[(warp * G + h) * D + 16 * mt + r0 + 8] = o[mt][2 + hh];
+        }
+        if (r0 == 0) {
+          m_sh[warp][h] = m_fin[hh];
+          l_sh[warp][h] = l_fin[hh];
+        }
+      }
+    }
+  } else if (r0 < G) {
 #pragma unroll
     for (int n = 0; n < 16; ++n) {
       acc_sh[(warp * G + r0) * D + n * 8 + cq] = o[n][0];
       acc_sh[(warp * G + r0) * D + n * 8 + cq + 1] = o[n][1];
     }
     if ((lane & 3) == 0) {
-      m_sh[warp][r0] = m0;
-      l_sh[warp][r0] = l0;
+      m_sh[warp][r0] = m_fin[0];
+      l_sh[warp][r0] = l_fin[0];
     }
   }
   __syncthreads();
@@ -1364,6 +1489,15 @@ static int v3_bwaves() {
   return w;
 }
 static int v3_per_sm() { return v3_stages() == 2 ? 3 : 2; }
+// v3 inner loop: transposed contractions (TF_ATTN_TR=1) or the original
+static bool v3_transposed() {
+  static int t = -1;
+  if (t < 0) {
+    const char* e = getenv("TF_ATTN_TR");
+    t = (e && e[0] == '1') ? 1 : 0;
+  }
+  return t == 1;
+}
 static int v3_l2_prefetch() {  // TF_ATTN_PF: blocks prefetched into L2 past the ring, per warp
   static int pf = -1;
   if (pf < 0) {
@@ -1409,16 +1543,23 @@ static int launch(const AttnArgs& a, int B, cudaStream_t st) {
     const int smem = kV3Warps * S * 2 * kBlk * kRowPad * 2;
     static bool attr3 = false;
     if (!attr3) {
-      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kV3Warps * 2 * 2 * kBlk * kRowPad * 2));
-      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kV3Warps * 3 * 2 * kBlk * kRowPad * 2));
+      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kV3Warps * 2 * 2 * kBlk * kRowPad * 2));
+      TF_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel<GG, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kV3Warps * 3 * 2 * kBlk * kRowPad * 2));
       attr3 = true;
     }
+    const bool tr = v3_transposed();
     if (S == 2)
-      paged_attn_mma_kernel<GG, 2><<<grid, kV3Warps * 32, smem, st>>>(a);
+      tr ? paged_attn_mma_kernel<GG, 2, true><<<grid, kV3Warps * 32, smem, st>>>(a)
+         : paged_attn_mma_kernel<GG, 2, false><<<grid, kV3Warps * 32, smem, st>>>(a);
     else
-      paged_attn_mma_kernel<GG, 3><<<grid, kV3Warps * 32, smem, st>>>(a);
+      tr ? paged_attn_mma_kernel<GG, 3, true><<<grid, kV3Warps * 32, smem, st>>>(a)
+         : paged_attn_mma_kernel<GG, 3, false><<<grid, kV3Warps * 32, smem, st>>>(a);
   } else if (attn_impl() >= 2) {
     const int smem = kStages * 2 * kBlk * D * 2;
     static bool attr = false;
