@@ -804,12 +804,13 @@ def cpu_baseline(args, timed, quick=False):
     reference simulator on the same C2 burst (1 core, per-call on_tick /
     plan_write_chunk / _snapshot), the policy's on_tick / select_batch at the
     selector's N, and the host's CPU model / NUMA layout."""
-    from oracle.cpu_baseline import host_info, time_cpu_step, time_reference_sim
+    from oracle.cpu_baseline import host_info, time_cpu_gather, time_cpu_step, time_reference_sim
 
     b = max(1, int(statistics.median([s["batch"] for s in timed])) if timed else 128)
     out = time_cpu_step(batch=b, ctx=2600, threads=os.cpu_count() or 1, seconds=args.cpu_seconds)
     out["reference_sim"] = time_reference_sim("c2_burst256_s1_tokenflow")
     out["host"] = host_info()
+    out["kv_gather_cpu"] = time_cpu_gather(threads=os.cpu_count() or 1)
     if not args.no_selector:
         sys.path.insert(0, str(ROOT / "tools"))
         from selector_latency import cpu_selector_latency
@@ -822,7 +823,7 @@ def run_reference(args):
     world, rank, _ = _dist()
     if rank != 0:
         return None
-    from oracle.cpu_baseline import host_info, time_cpu_step, time_reference_sim
+    from oracle.cpu_baseline import host_info, time_cpu_gather, time_cpu_step, time_reference_sim
 
     cb = time_cpu_step(batch=args.ref_batch, ctx=2600, threads=os.cpu_count() or 1, seconds=args.cpu_seconds)
     cb["reference_sim"] = time_reference_sim("c2_burst256_s1_tokenflow")

@@ -165,3 +165,30 @@ def time_cpu_step(batch: int = 64, ctx: int = 2600, threads: int = 16, seconds: 
             "sample": f"{n} single-layer passes of a B={batch}, ctx={ctx} Llama3-8B decode step (bf16 GEMMs + fp32 "
                       f"GQA attention) scaled x{S.n_layers} layers + lm_head + one step's swap gather + 1/"
                       f"{ticks_per_step:.0f} of an on_tick (oracle restatement); torch CPU, {threads} threads"}
+
+
+def time_cpu_gather(blocks: int = 256, pool_blocks: int = 512, threads: int = 16, reps: int = 5) -> dict:
+    """The unpinned byte path on the host: gather ``blocks``
+    random 2 MiB Llama3-8B KV blocks (all layers) out of a ``pool_blocks``
+    host-resident pool into a staging buffer and scatter them back - the
+    CPU restatement of tf_kv_gather_d2h / tf_kv_scatter_h2d on whole blocks,
+    torch index_select / index_copy_ on ``threads`` threads.  Bounded: a 1 GiB
+    pool, 512 MiB moved per direction per rep."""
+    torch.set_num_threads(threads)
+    elems = 32 * 2 * 8 * 16 * 128  # bf16 elements per block (2 MiB)
+    pool = torch.empty(pool_blocks, elems, dtype=torch.int16).random_()
+    stage = torch.empty(blocks, elems, dtype=torch.int16)
+    ids = torch.randperm(pool_blocks, generator=torch.Generator().manual_seed(0))[:blocks]
+    torch.index_select(pool, 0, ids, out=stage)  # warm-up (page faults)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        torch.index_select(pool, 0, ids, out=stage)
+    t_g = (time.perf_counter() - t0) / reps
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        pool.index_copy_(0, ids, stage)
+    t_s = (time.perf_counter() - t0) / reps
+    nbytes = blocks * elems * 2
+    return {"gather_gbs": round(nbytes / t_g / 1e9, 2), "scatter_gbs": round(nbytes / t_s / 1e9, 2),
+            "blocks": blocks, "block_bytes": elems * 2, "threads": threads,
+            "sample": f"{blocks} random 2 MiB blocks of a {pool_blocks}-block host pool, {reps} reps per direction"}
