@@ -435,8 +435,10 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": f"synthetic (random-init {shape.name} weights, seeded prompt token ids, frozen C2 trace)",
-        "config": {"workload": (f"C4: Qwen2.5-32B bf16 random-init, tensor-parallel TP={world} (NCCL all-reduce "
-                                f"after o_proj / down_proj), 256-request {args.arrivals} (C2 population), KV ledger "
+        "config": {"workload": (f"C4: Qwen2.5-32B bf16 random-init, tensor-parallel TP={world} ("
+                                + ("peer-memory all-reduce fused with residual + RMSNorm" if args.tp_data == "peer"
+                                   else "NCCL all-reduce") +
+                                f" after o_proj / down_proj), 256-request {args.arrivals} (C2 population), KV ledger "
                                 "163,840 tokens (40 GiB over the TP ranks) + pinned host tier per rank, block 16, "
                                 "max_batch 128") if tp_mode else
                                (f"C2: Llama3-8B bf16 random-init, 1xB200 per replica, 256-request {args.arrivals} "
