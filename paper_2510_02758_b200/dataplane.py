@@ -335,18 +335,18 @@ class GpuDataPlane:
                 if self.htab[rid][jj] < 0:
                     self.htab[rid][jj] = self.pool.alloc(TIER_HOST, 1)[0]
                     self._pending_htable.append((rid, jj, int(self.htab[rid][jj])))
-        pl = pos.tolist()
-        spans = [(rid, p, p + 1) for rid, p in zip(batch, pl)]
         self.stats["append_tokens"] += len(batch)
         self.stats["decode_steps"] += 1
-        self._wait_d2h_of(spans, self.s_compute)
+        busy = self._d2h_busy
+        if self.mode == "realtime" and busy is not None and busy[0] in batch:
+            self.s_compute.wait_event(busy[4])
         if self.model is not None and self.kv_source == "model":
             self._flush_table(self.s_compute)
             if self.fused_wt:
                 self._flush_htable(self.s_compute)
             self.model.decode(self, batch, eng)
         else:
-            self._write_kv(spans, self.s_compute)
+            self._write_kv([(rid, p, p + 1) for rid, p in zip(batch, pos.tolist())], self.s_compute)
             self._synthetic_attention(batch, eng)
 
     def decode_done(self, batch, made):

@@ -21,6 +21,7 @@ import math
 import os
 import time
 
+import numpy as np
 import torch
 from torch.nn.attention.varlen import varlen_attn
 
@@ -297,7 +298,7 @@ class PagedDecoder:
                 if job.kind == "recompute":
                     hist = torch.tensor(self.history.get(rid, []), dtype=torch.long)
                     toks = torch.cat([prompt, hist])[: hi - lo]
-                    if len(spans) == 1 and self._pgraphs and toks.numel() <= max(self._pgraphs):
+                    if len(spans) == 1 and self._prefill_fits_graph([(rid, toks, 0)]):
                         self._recompute_graph(dp, rid, toks, st)
                         return
                     seqs.append((rid, toks, 0))
@@ -306,7 +307,10 @@ class PagedDecoder:
                                               "use the synthetic KV source for that baseline")
                 else:
                     seqs.append((rid, prompt[lo: hi - 1], lo))
-            t0 = self._prefill_batch(dp, seqs, st)
+            if job.kind != "recompute" and self._prefill_fits_graph(seqs) and self.attn_timing is None:
+                t0 = self._prefill_graph(dp, seqs, st)
+            else:
+                t0 = self._prefill_batch(dp, seqs, st)
             if job.kind == "recompute":
                 return
             rids = [r for r, _, _ in seqs]
@@ -414,7 +418,7 @@ class PagedDecoder:
         return [(b, e0.elapsed_time(e1)) for b, e0, e1 in res]
 
     # ------------------------------------------------------------ CUDA graphs
-    def enable_graphs(self, dp, buckets=(8, 16, 24, 32, 48, 64, 80, 96, 112, 128), prefill_buckets=512):
+    def enable_graphs(self, dp, buckets=(8, 16, 24, 32, 48, 64, 80, 96, 112, 128), prefill_buckets=128):
         """Capture the decode forward once per batch-size bucket.
 
         Shapes are static per bucket: padded rows point at a scratch table row
@@ -450,22 +454,39 @@ class PagedDecoder:
         if prefill_buckets:
             self._capture_recompute_graphs(dp, mempool, st, prefill_buckets)
 
+    PF_SEQS = 8  # real sequences per captured prefill graph
+
+    @staticmethod
+    def _prefill_bucket_sizes(top, step):
+        """Token buckets of the prefill graphs: ``step``-token steps up to 1024,
+        2 x step up to 2048, 4 x step above (a 533-token prompt pads to 640,
+        not to 1024), capped at ``top``."""
+        out, T = [], 0
+        while T < top:
+            T += step if T < 1024 else (2 * step if T < 2048 else 4 * step)
+            out.append(min(T, top))
+        return sorted(set(out))
+
     def _capture_recompute_graphs(self, dp, mempool, st, step):
-        """Recompute prefills (one request re-prefilling its whole context,
-        engine.py:889-917) as CUDA graphs per token bucket of ``step`` tokens:
-        the host launches one graph instead of ~400 kernels, so the serving
-        loop stays responsive while the policy is recomputing.  The tail of a
-        bucket is a padding sequence written to the scratch row."""
+        """Prefills (prompt prefills of up to PF_SEQS requests, and recomputes:
+        one request re-prefilling its whole context, engine.py:889-917) as CUDA
+        graphs per token bucket: the host launches one graph instead of ~400
+        kernels (an eager 32-layer prefill costs ~10 ms of host time, longer
+        than the GPU needs for a 512-token prompt), so the serving loop stays
+        responsive.  Layout of a bucket of T tokens: the real sequences, then
+        one padding sequence on the scratch row up to T; cu_seqlens has a
+        fixed PF_SEQS + 2 entries (unused real slots are zero-length), and the
+        argmax is taken after each real sequence's last token."""
         self._pgraphs = {}
-        top = min(dp.max_len, dp.nlb * dp.B)
-        for T in range(step, top + step, step):
-            T = min(T, top)
+        NS = self.PF_SEQS
+        top = min(dp.max_len + NS, dp.nlb * dp.B)
+        for T in self._prefill_bucket_sizes(top, step):
             tok = torch.zeros(T, dtype=torch.int64, device=self.device)
-            meta = torch.zeros(2 * T + 3, dtype=torch.int32, device=self.device)
-            last = torch.full((1,), T - 1, dtype=torch.int64, device=self.device)
+            meta = torch.zeros(2 * T + NS + 2, dtype=torch.int32, device=self.device)
+            last = torch.zeros(NS, dtype=torch.int64, device=self.device)
             meta[:T] = dp.scratch_row
             meta[T:2 * T] = torch.arange(T, dtype=torch.int32, device=self.device)
-            meta[2 * T:] = torch.tensor([0, T, T], dtype=torch.int32, device=self.device)
+            meta[2 * T + NS + 1] = T  # all real slots empty, padding = [0, T)
             rows, pos32, cu = meta[:T], meta[T:2 * T], meta[2 * T:]
             with torch.cuda.stream(st):
                 self._prefill_core(dp, tok, rows, pos32, cu, T, last, st)  # warm-up
@@ -473,33 +494,56 @@ class PagedDecoder:
             g = torch.cuda.CUDAGraph()
             c0 = lib.tf_launch_count()
             with torch.cuda.graph(g, pool=mempool, stream=st):
-                self._prefill_core(dp, tok, rows, pos32, cu, T, last, torch.cuda.current_stream())
+                out = self._prefill_core(dp, tok, rows, pos32, cu, T, last, torch.cuda.current_stream())
             self._graph_launches[("recompute", T)] = lib.tf_launch_count() - c0
             stage_tok = torch.zeros(T, dtype=torch.int64, pin_memory=True)
-            stage_meta = torch.zeros(2 * T + 3, dtype=torch.int32, pin_memory=True)
-            self._pgraphs[T] = (g, tok, meta, last, stage_tok, stage_meta)
-            if T == top:
-                break
+            stage_meta = torch.zeros(2 * T + NS + 2, dtype=torch.int32, pin_memory=True)
+            stage_last = torch.zeros(NS, dtype=torch.int64, pin_memory=True)
+            self._pgraphs[T] = (g, tok, meta, last, stage_tok, stage_meta, stage_last, out)
         st.synchronize()
 
-    def _recompute_graph(self, dp, rid, toks, st):
-        n = toks.numel()
+    def _prefill_fits_graph(self, seqs) -> bool:
+        if not self._pgraphs or len(seqs) > self.PF_SEQS or any(p0 != 0 for _, _, p0 in seqs):
+            return False
+        return sum(t.numel() for _, t, _ in seqs) <= max(self._pgraphs)
+
+    def _prefill_graph(self, dp, seqs, st):
+        """Replay the prefill graph of the smallest bucket that holds ``seqs``
+        = [(rid, tokens[int64 cpu], 0)]; returns the argmax after each
+        sequence's last token (a view of the graph's static output)."""
+        NS = self.PF_SEQS
+        lens = [t.numel() for _, t, _ in seqs]
+        n = sum(lens)
         T = next(b for b in sorted(self._pgraphs) if b >= n)
-        g, tok, meta, last, stage_tok, stage_meta = self._pgraphs[T]
-        stage_tok[:n] = toks
-        stage_tok[n:] = 0
-        stage_meta[:n] = rid
-        stage_meta[n:T] = dp.scratch_row
-        stage_meta[T:T + n] = torch.arange(n, dtype=torch.int32)
-        stage_meta[T + n:2 * T] = torch.arange(T - n, dtype=torch.int32)
-        stage_meta[2 * T:] = torch.tensor([0, n, T], dtype=torch.int32)
+        g, tok, meta, last, stage_tok, stage_meta, stage_last, out = self._pgraphs[T]
+        st_tok, st_meta, st_last = stage_tok.numpy(), stage_meta.numpy(), stage_last.numpy()
+        st_tok[:n] = torch.cat([t for _, t, _ in seqs]).numpy()
+        st_tok[n:] = 0
+        cu = np.zeros(NS + 2, np.int32)
+        o = 0
+        for i, ((rid, _, _), ln) in enumerate(zip(seqs, lens)):
+            st_meta[o:o + ln] = rid
+            st_meta[T + o:T + o + ln] = np.arange(ln, dtype=np.int32)
+            o += ln
+            cu[i + 1] = o
+            st_last[i] = o - 1
+        cu[len(seqs) + 1:NS + 1] = o  # unused real slots: zero-length
+        cu[NS + 1] = T                # the padding sequence [n, T) on the scratch row
+        st_last[len(seqs):] = 0
+        st_meta[n:T] = dp.scratch_row
+        st_meta[T + n:2 * T] = np.arange(T - n, dtype=np.int32)
+        st_meta[2 * T:] = cu
         with torch.cuda.stream(st):
-            for dst, src in ((tok, stage_tok), (meta, stage_meta)):
+            for dst, src in ((tok, stage_tok), (meta, stage_meta), (last, stage_last)):
                 check(lib.tf_copy_small(C.c_void_p(dst.data_ptr()), C.c_void_p(src.data_ptr()),
                                         dst.numel() * dst.element_size(), C.c_void_p(st.cuda_stream)),
                       "tf_copy_small")
             g.replay()
             self.replayed_launches += self._graph_launches.get(("recompute", T), 0)
+        return out[: len(seqs)]
+
+    def _recompute_graph(self, dp, rid, toks, st):
+        self._prefill_graph(dp, [(rid, toks, 0)], st)
 
     def _forward_graphable(self, dp, io, Bp, ws, st):
         rows = io[1].to(torch.int32)
@@ -514,12 +558,20 @@ class PagedDecoder:
         B = len(rids)
         Bp = next(b for b in sorted(self._graphs) if b >= B)
         g, io, stage, out, _ = self._graphs[Bp]
-        stage[0, :B] = 0 if tokens_dev is not None else torch.tensor([self.pending[r] for r in rids])
-        stage[0, B:] = 0
-        stage[1, :B] = torch.tensor(rids)
-        stage[1, B:] = dp.scratch_row
-        stage[2, :B] = torch.tensor(positions)
-        stage[2, B:] = 0
+        # numpy view of the pinned staging rows: list -> int64 row writes cost a
+        # few us each, torch.tensor(list) + slice copies ~4x that (host time
+        # here sits between a step's completion and the next step's launch)
+        sn = stage.numpy()
+        if tokens_dev is not None:
+            sn[0, :B] = 0
+        else:
+            pend = self.pending
+            sn[0, :B] = [pend[r] for r in rids]
+        sn[0, B:] = 0
+        sn[1, :B] = rids
+        sn[1, B:] = dp.scratch_row
+        sn[2, :B] = positions
+        sn[2, B:] = 0
         with torch.cuda.stream(st):
             # zero-copy read of the pinned staging row (not a copy-engine H2D:
             # those queue behind KV loads on the same engine)

@@ -208,6 +208,60 @@ def test_recompute_prefill_graph_matches_eager(cuda):
     assert (a - b).abs().max().item() <= 2e-2 * max(1.0, a.abs().max().item())
 
 
+def test_prompt_prefill_graph_matches_eager(cuda):
+    """A multi-request prompt prefill replayed from its token-bucket CUDA graph
+    (real sequences, zero-length unused slots, a padding sequence on the
+    scratch row) writes the same paged KV as the eager varlen prefill and
+    picks the same first tokens wherever the eager logits are not a near tie."""
+    import torch
+
+    from paper_2510_02758_b200 import configs
+    from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
+    from paper_2510_02758_b200.model import PagedDecoder
+    from paper_2510_02758_b200.workload import RequestSpec
+
+    shape = configs.TINY
+    n_req, nlb = 3, 8
+    reqs = [RequestSpec(i, 0.0, 90, 30, 20.0) for i in range(n_req)]
+    g = torch.Generator().manual_seed(11)
+    seqs = [(i, torch.randint(0, shape.vocab, (n,), generator=g), 0) for i, n in enumerate((37, 90, 5))]
+    res = []
+    for use_graph in (False, True):
+        pool = KvPool(n_req * nlb + 4, 1, shape.n_layers, shape.n_kv_heads, shape.head_dim, device=cuda)
+        pool.gpu.zero_()
+        model = PagedDecoder(shape, device=cuda, seed=5)
+        dp = GpuDataPlane(reqs, pool, mode="realtime", kv_source="model", model=model, n_q_heads=shape.n_q_heads)
+        dp.enable_scratch()
+        free = [b for b in range(pool.n_blocks) if b != dp.scratch_block]
+        dp.table[:n_req, :nlb] = torch.tensor(free[: n_req * nlb], dtype=torch.int32, device=cuda).view(n_req, nlb)
+        st = dp.s_compute
+        if use_graph:
+            model.enable_graphs(dp, buckets=(8,), prefill_buckets=32)
+            assert model._prefill_fits_graph(seqs)
+            with torch.cuda.stream(st):
+                tok = model._prefill_graph(dp, seqs, st).clone()
+        else:
+            model.keep_logits = True
+            with torch.cuda.stream(st):
+                tok = model._prefill_batch(dp, seqs, st)
+            logits = model.last_logits.float()
+        torch.cuda.synchronize()
+        kv = []
+        for rid, t, _ in seqs:
+            n = t.numel()
+            blocks = dp.table[rid, : (n + 15) // 16].long()
+            v = pool.gpu_view()[blocks].view(torch.bfloat16).float()
+            v = v.permute(0, 4, 1, 2, 3, 5).reshape(-1, shape.n_layers, 2, shape.n_kv_heads, shape.head_dim)[:n]
+            kv.append(v)
+        res.append((tok, kv))
+    (t_e, kv_e), (t_g, kv_g) = res
+    for a, b in zip(kv_e, kv_g):
+        assert (a - b).abs().max().item() <= 2e-2 * max(1.0, a.abs().max().item())
+    top2 = logits.topk(2, dim=-1).values
+    clear = (top2[:, 0] - top2[:, 1]) > 2e-2 * logits.abs().amax(-1) * 2
+    assert torch.equal(t_e[clear], t_g[clear])
+
+
 def _tp2_worker(rank, port, out):
     import os
 
