@@ -28,6 +28,8 @@ from torch.nn.attention.varlen import varlen_attn
 from . import _lib
 from ._lib import check, lib
 
+_DEBUG_GRAPHS = os.environ.get("TF_DEBUG_GRAPHS") == "1"  # sync + range-check every graph replay (debug)
+
 
 class _Staging:
     """Grow-only pinned host + device buffer for a host -> device input:
@@ -105,6 +107,7 @@ class PagedDecoder:
         self.pending = {}  # rid -> next token to emit
         self.history = {}  # rid -> generated tokens (for recompute)
         self.keep_logits, self.last_logits, self.graph_logits = False, None, {}
+        self._stage_ev, self.stage_waits = {}, 0
         self.lpt_order = os.environ.get("TF_LPT", "0") == "1"  # decode rows longest-context first
         self.prompts = {}
         self._unresolved = {}  # rid -> (pinned buffer, column) of an in-flight prefill's t0/t1
@@ -510,12 +513,13 @@ class PagedDecoder:
     def _prefill_graph(self, dp, seqs, st):
         """Replay the prefill graph of the smallest bucket that holds ``seqs``
         = [(rid, tokens[int64 cpu], 0)]; returns the argmax after each
-        sequence's last token (a view of the graph's static output)."""
+        sequence's last token (copied out of the graph's static output)."""
         NS = self.PF_SEQS
         lens = [t.numel() for _, t, _ in seqs]
         n = sum(lens)
         T = next(b for b in sorted(self._pgraphs) if b >= n)
         g, tok, meta, last, stage_tok, stage_meta, stage_last, out = self._pgraphs[T]
+        self._stage_guard(("p", T))
         st_tok, st_meta, st_last = stage_tok.numpy(), stage_meta.numpy(), stage_last.numpy()
         st_tok[:n] = torch.cat([t for _, t, _ in seqs]).numpy()
         st_tok[n:] = 0
@@ -538,12 +542,41 @@ class PagedDecoder:
                 check(lib.tf_copy_small(C.c_void_p(dst.data_ptr()), C.c_void_p(src.data_ptr()),
                                         dst.numel() * dst.element_size(), C.c_void_p(st.cuda_stream)),
                       "tf_copy_small")
+            self._stage_mark(("p", T), st)
             g.replay()
             self.replayed_launches += self._graph_launches.get(("recompute", T), 0)
-        return out[: len(seqs)]
+        if _DEBUG_GRAPHS:
+            st.synchronize()
+            tv, lv, mv = tok.cpu(), last.cpu(), meta.cpu()
+            assert 0 <= int(tv.min()) and int(tv.max()) < self.s.vocab, ("prefill tok", T, n, tv.tolist()[:n + 4])
+            assert 0 <= int(lv.min()) and int(lv.max()) < T, ("prefill last", T, lv.tolist())
+            assert torch.equal(tv[:n], stage_tok[:n]) and torch.equal(mv, stage_meta), ("prefill stage", T, n)
+            ov = out[: len(seqs)].cpu()
+            assert 0 <= int(ov.min()) and int(ov.max()) < self.s.vocab, ("prefill out", ov.tolist())
+        # copied out of the graph pool before any other graph replays: all graphs
+        # share one memory pool, and a graph captured EARLIER (the decode graph
+        # that samples t1 next) may reuse this output's addresses for its own
+        # intermediates
+        with torch.cuda.stream(st):
+            return out[: len(seqs)].clone()
 
     def _recompute_graph(self, dp, rid, toks, st):
         self._prefill_graph(dp, [(rid, toks, 0)], st)
+
+    def _stage_guard(self, key):
+        """A pinned staging buffer is rewritten only after the GPU read its
+        previous contents (the zero-copy tf_copy_small of the last replay that
+        used it); counts the times the host actually had to wait."""
+        ev = self._stage_ev.get(key)
+        if ev is not None and not ev.query():
+            self.stage_waits += 1
+            ev.synchronize()
+
+    def _stage_mark(self, key, st):
+        ev = self._stage_ev.get(key)
+        if ev is None:
+            ev = self._stage_ev[key] = torch.cuda.Event()
+        ev.record(st)
 
     def _forward_graphable(self, dp, io, Bp, ws, st):
         rows = io[1].to(torch.int32)
@@ -558,6 +591,7 @@ class PagedDecoder:
         B = len(rids)
         Bp = next(b for b in sorted(self._graphs) if b >= B)
         g, io, stage, out, _ = self._graphs[Bp]
+        self._stage_guard(("d", Bp))
         # numpy view of the pinned staging rows: list -> int64 row writes cost a
         # few us each, torch.tensor(list) + slice copies ~4x that (host time
         # here sits between a step's completion and the next step's launch)
@@ -577,10 +611,17 @@ class PagedDecoder:
             # those queue behind KV loads on the same engine)
             check(lib.tf_copy_small(C.c_void_p(io.data_ptr()), C.c_void_p(stage.data_ptr()),
                                     io.numel() * io.element_size(), C.c_void_p(st.cuda_stream)), "tf_copy_small")
+            self._stage_mark(("d", Bp), st)
             if tokens_dev is not None:
                 io[0, :B].copy_(tokens_dev)
             g.replay()
             self.replayed_launches += self._graph_launches.get(("decode", Bp), 0)
+        if _DEBUG_GRAPHS:
+            st.synchronize()
+            iv = io.cpu()
+            assert 0 <= int(iv[0].min()) and int(iv[0].max()) < self.s.vocab, ("decode tokens", Bp, B, iv[0].tolist(),
+                                                                            tokens_dev is not None)
+            assert torch.equal(iv[1:], stage[1:]), ("decode stage rows/pos", Bp, B)
         # the staging buffer is reused next step only after this step completed
         return out[:B]
 
