@@ -327,9 +327,19 @@ class GpuDataPlane:
         self.flags[rids, pos] |= RESERVED
         self._appending.update(zip(batch, pos.tolist()))
         j = pos // self.B
-        need = (pos % self.B == 0) | (self.gtab[rids, j] < 0)
-        for rid, jj in zip(rids[need].tolist(), j[need].tolist()):
-            self._reconcile(rid, [jj])
+        # a member whose new position opens an unmapped logical block gets a
+        # fresh block: one allocator call for all of them, handed out in batch
+        # order - exactly the blocks per-member reconciles would pop from the
+        # LIFO stack (nothing is freed here: the block was unmapped), at a
+        # fraction of the host time (every 16th step all B members grow)
+        grow = self.gtab[rids, j] < 0
+        if grow.any():
+            r_g, j_g = rids[grow], j[grow]
+            ids = self._alloc_blocks(int(grow.sum()))
+            self.gtab[r_g, j_g] = ids
+            self._pending_table.extend(zip(r_g.tolist(), j_g.tolist(), ids))
+            used = self.pool.n_blocks - self.pool.free_count(TIER_GPU) - self._q_blocks
+            self.peak_blocks = max(self.peak_blocks, used)
         if self.fused_wt:
             for rid, jj in zip(batch, j.tolist()):
                 if self.htab[rid][jj] < 0:
