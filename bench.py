@@ -293,21 +293,21 @@ def run_ours(args):
                                  "the window on the running batch with the plan the decode graphs replay (batch "
                                  "padded to its bucket with scratch rows, max_ctx = the pool maximum)"}
         if args.graphs:
-            xf = dp.transfer_log()[state["ev0"]:state["ev1"]]
-            per_step = lambda k: math.ceil(sum(n for d, n, _ in xf if d == k) / 16 / len(timed))  # noqa: E731
-            hid_w = measure_hidden(model, dp, eng, live, per_step("d2h"), per_step("h2d"))
+            hid_m = measure_hidden_mix(model, dp, eng, live, state["ev0"], state["ev1"], len(timed),
+                                       args.swap_engine)
             # blocks per direction that keep the duplex link (~45 GB/s each way
             # when both run) busy for ~80% of one decode step: the transfer CAN
             # then be hidden completely, so the fraction measures overlap quality
-            sat = max(1, int(0.8 * 45e9 * (hid_w["t_decode_ms"] if hid_w else 7.0) / 1e3 / dp.pool.block_bytes))
+            t_dec = hid_m["t_decode_ms"] if hid_m else 7.0
+            sat = max(1, int(0.8 * 45e9 * t_dec / 1e3 / dp.pool.block_bytes))
             hid_s = measure_hidden(model, dp, eng, live, sat, sat)
-            hid_m = measure_hidden_mix(model, dp, eng, live, state["ev0"], state["ev1"], len(timed),
-                                       args.swap_engine)
-            state["hidden"] = {"window_mix": hid_m, "window_volume": hid_w, "link_saturating": hid_s,
+            state["hidden"] = {"window_mix": hid_m, "link_saturating": hid_s,
                                "note": "hidden = 1 - (T_both - T_decode)/T_swap; decode = the captured forward of "
-                                       "the live batch; window_mix replays the window's own chunks (their segment "
-                                       "shapes, the serving engine) per step; window_volume / link_saturating move "
-                                       "whole blocks on the copy engines"}
+                                       "the live batch; window_mix replays the window's own chunks (segment shapes, "
+                                       "engine, order) scaled to ~50% of a decode step; link_saturating moves whole "
+                                       "blocks both ways sized to ~80% of a decode step (the window's own volume, "
+                                       "~0.1-0.3 ms of copies per step, is below the step-to-step noise of "
+                                       "T_decode)"}
         if not args.no_selector:
             sys.path.insert(0, str(ROOT / "tools"))
             from selector_latency import gpu_selector_latency
