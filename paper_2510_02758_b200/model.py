@@ -523,20 +523,7 @@ class PagedDecoder:
         st_tok, st_meta, st_last = stage_tok.numpy(), stage_meta.numpy(), stage_last.numpy()
         st_tok[:n] = torch.cat([t for _, t, _ in seqs]).numpy()
         st_tok[n:] = 0
-        cu = np.zeros(NS + 2, np.int32)
-        o = 0
-        for i, ((rid, _, _), ln) in enumerate(zip(seqs, lens)):
-            st_meta[o:o + ln] = rid
-            st_meta[T + o:T + o + ln] = np.arange(ln, dtype=np.int32)
-            o += ln
-            cu[i + 1] = o
-            st_last[i] = o - 1
-        cu[len(seqs) + 1:NS + 1] = o  # unused real slots: zero-length
-        cu[NS + 1] = T                # the padding sequence [n, T) on the scratch row
-        st_last[len(seqs):] = 0
-        st_meta[n:T] = dp.scratch_row
-        st_meta[T + n:2 * T] = np.arange(T - n, dtype=np.int32)
-        st_meta[2 * T:] = cu
+        st_meta[:], st_last[:] = self.prefill_layout([r for r, _, _ in seqs], lens, T, NS, dp.scratch_row)
         with torch.cuda.stream(st):
             for dst, src in ((tok, stage_tok), (meta, stage_meta), (last, stage_last)):
                 check(lib.tf_copy_small(C.c_void_p(dst.data_ptr()), C.c_void_p(src.data_ptr()),
@@ -559,6 +546,34 @@ class PagedDecoder:
         # intermediates
         with torch.cuda.stream(st):
             return out[: len(seqs)].clone()
+
+    @staticmethod
+    def prefill_layout(rids, lens, T, NS, scratch_row):
+        """Device inputs of a prefill graph of T tokens for sequences of
+        ``lens`` tokens (request ``rids``): meta = [row of every token | its
+        position | cu_seqlens (NS + 2 entries)] and the index of each
+        sequence's last token (NS entries).  The real sequences come first,
+        unused sequence slots are zero-length, and the padding sequence
+        [sum(lens), T) sits on the scratch row."""
+        n = sum(lens)
+        if len(lens) > NS or n > T:
+            raise ValueError(f"{len(lens)} sequences / {n} tokens do not fit a {T}-token graph with {NS} slots")
+        meta = np.empty(2 * T + NS + 2, np.int32)
+        last = np.zeros(NS, np.int64)
+        cu = meta[2 * T:]
+        cu[0] = 0
+        o = 0
+        for i, (rid, ln) in enumerate(zip(rids, lens)):
+            meta[o:o + ln] = rid
+            meta[T + o:T + o + ln] = np.arange(ln, dtype=np.int32)
+            o += ln
+            cu[i + 1] = o
+            last[i] = o - 1
+        cu[len(lens) + 1:NS + 1] = o  # unused real slots: zero-length
+        cu[NS + 1] = T                # the padding sequence [n, T) on the scratch row
+        meta[n:T] = scratch_row
+        meta[T + n:2 * T] = np.arange(T - n, dtype=np.int32)
+        return meta, last
 
     def _recompute_graph(self, dp, rid, toks, st):
         self._prefill_graph(dp, [(rid, toks, 0)], st)

@@ -208,3 +208,32 @@ def test_bench_helpers():
     assert s["complete"] and s["requests"] == 100
     assert s["p99_s"] == metrics.nearest_rank(v, 99.0) and s["p50_s"] == metrics.nearest_rank(v, 50.0)
     assert bench._ttft_summary([], 5, 1, False) is None
+
+
+def test_prefill_graph_layout():
+    """Host-side layout of a captured prefill graph: real sequences first,
+    zero-length unused slots, the padding sequence on the scratch row; every
+    token's row / position, the cu_seqlens and the last-token indices."""
+    import numpy as np
+
+    from paper_2510_02758_b200.model import PagedDecoder
+
+    T, NS, scratch = 64, 4, 99
+    meta, last = PagedDecoder.prefill_layout([7, 3], [10, 5], T, NS, scratch)
+    rows, pos, cu = meta[:T], meta[T:2 * T], meta[2 * T:]
+    assert cu.tolist() == [0, 10, 15, 15, 15, 64]
+    assert last.tolist() == [9, 14, 0, 0]
+    assert (rows[:10] == 7).all() and (rows[10:15] == 3).all() and (rows[15:] == scratch).all()
+    assert pos[:10].tolist() == list(range(10)) and pos[10:15].tolist() == list(range(5))
+    assert pos[15:].tolist() == list(range(T - 15))
+    # exactly full: the padding sequence is empty
+    meta, last = PagedDecoder.prefill_layout([1, 2, 3, 4], [16, 16, 16, 16], T, NS, scratch)
+    assert meta[2 * T:].tolist() == [0, 16, 32, 48, 64, 64] and last.tolist() == [15, 31, 47, 63]
+    with pytest.raises(ValueError):
+        PagedDecoder.prefill_layout([1, 2, 3, 4, 5], [1] * 5, T, NS, scratch)
+    with pytest.raises(ValueError):
+        PagedDecoder.prefill_layout([1], [65], T, NS, scratch)
+    b = PagedDecoder._prefill_bucket_sizes(4700, 128)
+    assert b[:8] == [128 * i for i in range(1, 9)] and b[-1] == 4700 and b == sorted(set(b))
+    assert all(y - x <= 512 for x, y in zip(b, b[1:]))
+    assert np.all(np.diff(b) > 0)

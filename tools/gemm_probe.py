@@ -39,7 +39,10 @@ def time_graph(fn, reps=200):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/gemm_probe.json")
+    ap.add_argument("--blas", default="default", choices=["default", "cublas", "cublaslt"])
     args = ap.parse_args()
+    if args.blas != "default":
+        torch.backends.cuda.preferred_blas_library(args.blas)
     dev = torch.device("cuda")
     bf = torch.bfloat16
     rows = []
@@ -63,7 +66,7 @@ def main():
 
             t_mm, t_add = time_graph(mm), time_graph(addmm)
             wbytes = K * N * 2
-            rows.append({"M": M, "gemm": name, "K": K, "N": N, "mm_us": round(t_mm, 2), "addmm_us": round(t_add, 2),
+            rows.append({"blas": args.blas, "M": M, "gemm": name, "K": K, "N": N, "mm_us": round(t_mm, 2), "addmm_us": round(t_add, 2),
                          "mm_gbs": round(wbytes / t_mm / 1e3, 1), "addmm_gbs": round(wbytes / t_add / 1e3, 1)})
             print(json.dumps(rows[-1]), flush=True)
             del ws
