@@ -569,7 +569,7 @@ def _attn_kernel_name(shape, batch, graphs):
     if impl == 0:
         impl = 3
     return {1: "paged_attn_kernel (v1, CUDA cores)", 2: "paged_attn_tma_kernel (v2, bulk copy)",
-            3: f"paged_attn_mma_kernel<{G}> (v3, split-KV cp.async + mma.sync) + combine",
+            3: f"paged_attn_mma_kernel<{G}> (v3, split-KV cp.async + mma.sync, in-kernel split merge)",
             4: f"paged_attn_stream_kernel<{G}> (v4 stream-K)",
             5: f"paged_attn_tma5_kernel<{G}> (v5, TMA tensor loads + stream-K)"}[impl]
 

@@ -173,6 +173,30 @@ def test_paged_attention_parity_catches_a_dropped_split(cuda, impl):
     assert ratio > 1.0, f"mutated kernel passed the parity check (ratio {ratio:.2f})"
 
 
+@pytest.mark.parametrize("knob", ["TF_ATTN_TR=1", "TF_ATTN_BALANCED=1", "TF_ATTN_PF=2", "TF_ATTN_STAGES=3",
+                                  "TF_ATTN_STAGES=2"])
+def test_paged_attention_opt_in_variants_vs_fp32(cuda, knob):
+    """The measured-but-not-default v3 variants (transposed inner loop,
+    device-balanced split plan, L2 prefetch, forced ring depth) stay within
+    the parity tolerance; each runs in a subprocess because the library reads
+    its knobs once per process."""
+    import os
+    import subprocess
+    import sys
+
+    k, v = knob.split("=")
+    code = ("import sys; sys.path.insert(0, 'tests'); from attn_parity import run; import numpy as np; "
+            "rng = np.random.default_rng(9); "
+            "print(max(run(c, 4, 8, 32, 128, 1, impl=3) for c in ("
+            "[int(x) for x in rng.integers(1, 3000, 64)], [int(x) for x in rng.integers(200, 900, 128)], "
+            "[1, 15, 16, 17, 2049, 4000])))")
+    res = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **{k: v}), capture_output=True,
+                         text=True, timeout=300, cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    assert res.returncode == 0, res.stderr[-2000:]
+    ratio = float(res.stdout.strip().splitlines()[-1])
+    assert ratio <= 1.0, f"{knob}: worst row error is {ratio:.2f}x the tolerance"
+
+
 def test_paged_attention_workspace_reuse_is_deterministic(cuda):
     """The stream-K merge counters reset themselves: relaunching with the same
     workspace gives bit-identical outputs (merge order is fixed by slot)."""
