@@ -604,15 +604,16 @@ def _ttft_summary(recs, n_records, world, tp_mode):
 def _ncu_traffic(alg_bytes):
     """DRAM bytes per launch for the attention kernel: the DRAM-traffic /
     algorithmic-bytes ratio of the committed ncu --set full capture of the
-    same kernel (profiles/r1_attn_ncu_v3_v4.json) at the closest launch size,
+    same kernel (profiles/r2_attn_ncu_live.json, r1_attn_ncu_v3_v4.json) at the closest launch size,
     applied to this launch's algorithmic bytes."""
-    p = ROOT / "profiles" / "r1_attn_ncu_v3_v4.json"
     impl = os.environ.get("TF_ATTN_IMPL", "3")[:1]
     want = "stream" if impl == "4" else "mma"
-    try:
-        caps = [k for k in json.loads(p.read_text())["kernels"] if want in k["kernel"]]
-    except (OSError, ValueError, KeyError):
-        return None, None
+    caps = []
+    for name in ("r2_attn_ncu_live.json", "r1_attn_ncu_v3_v4.json"):
+        try:
+            caps += [k for k in json.loads((ROOT / "profiles" / name).read_text())["kernels"] if want in k["kernel"]]
+        except (OSError, ValueError, KeyError):
+            pass
     if not caps:
         return None, None
     k = min(caps, key=lambda c: abs(math.log(c["algorithmic_bytes"] / alg_bytes)))
