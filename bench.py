@@ -278,15 +278,23 @@ def run_ours(args):
         if not live:
             return
         plan = "graph" if args.graphs else "exact"
-        per = model.measure_attention(dp, live, [eng.state[r].kv.total_kv - 1 for r in live], plan=plan)
-        avg_ms = sum(ms for _, ms in per) / len(per)
+        per = model.measure_attention(dp, live, [eng.state[r].kv.total_kv - 1 for r in live], plan=plan,
+                                      graph_reps=5)
+        ev_ms = sum(ms for _, ms in per) / len(per)
         avg_bytes = sum(b for b, _ in per) / len(per)
+        # headline: the launches as the decode graphs run them (all layers back
+        # to back inside one CUDA graph, one event pair around 5 replays);
+        # beside it the same launches each bracketed by its own event pair
+        avg_ms = model.attn_graph_ms or ev_ms
         ach = avg_bytes / (avg_ms / 1e3) / 1e9
         traffic, tsrc = _ncu_traffic(avg_bytes)
         state["roof"] = {"bound": "hbm", "kernel": _attn_kernel_name(shape, len(live), bool(args.graphs)),
                          "achieved": round(ach, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(ach / hbm, 4), "traffic": traffic, "traffic_source": tsrc,
                          "launches": len(per), "avg_ms": round(avg_ms, 4), "batch": len(live), "plan": plan,
+                         "timing": "CUDA graph of the 32 layers' launches, 5 replays, one event pair",
+                         "avg_ms_per_launch_events": round(ev_ms, 4),
+                         "frac_per_launch_events": round(avg_bytes / (ev_ms / 1e3) / 1e9 / hbm, 4),
                          "algorithmic_bytes_per_launch": round(avg_bytes),
                          "note": f"bytes = sum(ctx) x {pool.H * pool.D * 4} B (K+V, {pool.H} kv heads x {pool.D} x "
                                  "bf16) + q/out + table entries per layer (real rows only); re-launched right after "

@@ -108,6 +108,7 @@ class PagedDecoder:
         self.history = {}  # rid -> generated tokens (for recompute)
         self.keep_logits, self.last_logits, self.graph_logits = False, None, {}
         self._stage_ev, self.stage_waits = {}, 0
+        self.attn_graph_ms = None  # measure_attention(graph_reps=...): avg launch inside a CUDA graph
         self.lpt_order = os.environ.get("TF_LPT", "0") == "1"  # decode rows longest-context first
         self.prompts = {}
         self._unresolved = {}  # rid -> (pinned buffer, column) of an in-flight prefill's t0/t1
@@ -372,14 +373,17 @@ class PagedDecoder:
                 self.pending[rid] = t
 
     @torch.no_grad()
-    def measure_attention(self, dp, rids, positions, reps=3, plan="exact"):
+    def measure_attention(self, dp, rids, positions, reps=3, plan="exact", graph_reps=0):
         """Time the paged-attention kernel on a live batch (all layers, CUDA
         events on the launching stream) -> [(algorithmic bytes, ms)] per launch.
 
         plan="graph" launches it exactly as the captured decode graphs do: the
         batch padded to its bucket with scratch rows (ctx 1) and max_ctx = the
         pool's maximum context; plan="exact" uses B and max(ctx).  The
-        algorithmic bytes count the real rows only."""
+        algorithmic bytes count the real rows only.  With
+        ``graph_reps`` the layers are also captured into one CUDA graph and
+        replayed: the average launch duration as in the decode graphs is left
+        in ``self.attn_graph_ms``."""
         s = self.s
         st = dp.s_compute
         B = len(rids)
@@ -417,7 +421,31 @@ class PagedDecoder:
                     e1.record(st)
                     if r > 0:  # first pass is warm-up
                         res.append((abytes, e0, e1))
+            per_launch = None
+            if graph_reps:
+                # the same launches as they run inside the decode graphs: all
+                # layers back to back in one CUDA graph, one event pair around
+                # graph_reps replays (no host, no per-launch event in between)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    for li in range(s.n_layers):
+                        check(lib.tf_paged_decode_attn(dp.pool.handle, C.c_void_p(q.data_ptr()),
+                                                       C.c_void_p(dp.table.data_ptr()), dp.nlb,
+                                                       C.c_void_p(rows.data_ptr()), C.c_void_p(ctx.data_ptr()), Bl,
+                                                       max_ctx, li, self.hq, self.scale, C.c_void_p(out.data_ptr()),
+                                                       C.c_void_p(ws.data_ptr()), ws_n,
+                                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                              "tf_paged_decode_attn")
+                g.replay()
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                g0.record(st)
+                for _ in range(graph_reps):
+                    g.replay()
+                g1.record(st)
         st.synchronize()
+        if graph_reps:
+            per_launch = g0.elapsed_time(g1) / (graph_reps * s.n_layers)
+            self.attn_graph_ms = per_launch
         return [(b, e0.elapsed_time(e1)) for b, e0, e1 in res]
 
     # ------------------------------------------------------------ CUDA graphs
