@@ -7,11 +7,11 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}
 tail -n 2 gpurun_out/${T}_smoke.log
 t0=$(date +%s); timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/${T}_bench20.json 2> gpurun_out/${T}_bench20.err; echo "rc=$? wall=$(( $(date +%s) - t0 ))s" >> gpurun_out/${T}_bench20.err
 t0=$(date +%s); timeout 900 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "rc=$? wall=$(( $(date +%s) - t0 ))s" >> gpurun_out/${T}_bench.err
-t0=$(date +%s); timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${T}_ref.json 2> gpurun_out/${T}_ref.err; echo "rc=$? wall=$(( $(date +%s) - t0 ))s" >> gpurun_out/${T}_ref.err
+t0=$(date +%s); timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${T}_ref.json 2> gpurun_out/${T}_ref.err; echo "rc=$? wall=$(( $(date +%s) - t0 ))s" >> gpurun_out/${T}_ref.err
 tail -n 1 gpurun_out/${T}_bench20.err gpurun_out/${T}_bench.err gpurun_out/${T}_ref.err
 python - <<'PY'
 import json
-for f in ("gpurun_out/${T}_bench20.json", "gpurun_out/${T}_bench.json"):
+for f in ("gpurun_out/r2t_bench20.json", "gpurun_out/r2t_bench.json"):
     try:
         d = json.load(open(f))
     except Exception as e:
@@ -21,5 +21,5 @@ for f in ("gpurun_out/${T}_bench20.json", "gpurun_out/${T}_bench.json"):
           "roof", (d.get("roofline") or {}).get("frac"), "d2h", d["swap"].get("d2h_gbs"), "h2d", d["swap"].get("h2d_gbs"),
           "hidden", {k: (v or {}).get("hidden_frac") for k, v in h.items() if isinstance(v, dict)},
           "mean_batch", d["config"]["mean_batch"], "clocks", d.get("clocks"))
-print(open("gpurun_out/${T}_ref.json").read()[:600])
+print(open("gpurun_out/r2t_ref.json").read()[:600])
 PY
