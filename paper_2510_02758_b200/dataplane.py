@@ -34,6 +34,8 @@ from __future__ import annotations
 import ctypes as C
 from collections import deque
 
+import os
+
 import numpy as np
 import torch
 
@@ -41,6 +43,7 @@ from . import _lib
 from ._lib import TIER_GPU, TIER_HOST, TfSeg, TfSpan, check, lib
 
 LIVE, DETACHED, RESERVED, HOSTV = np.uint8(1), np.uint8(2), np.uint8(4), np.uint8(8)
+_GROW_BATCH = os.environ.get("TF_GROW_BATCH", "1") != "0"  # A/B switch for the batched decode-growth allocation
 CLR_LIVE, CLR_DETACHED, CLR_RESERVED, CLR_HOSTV = np.uint8(0xFE), np.uint8(0xFD), np.uint8(0xFB), np.uint8(0xF7)
 
 
@@ -333,7 +336,10 @@ class GpuDataPlane:
         # LIFO stack (nothing is freed here: the block was unmapped), at a
         # fraction of the host time (every 16th step all B members grow)
         grow = self.gtab[rids, j] < 0
-        if grow.any():
+        if grow.any() and not _GROW_BATCH:
+            for rid, jj in zip(rids[grow].tolist(), j[grow].tolist()):
+                self._reconcile(rid, [jj])
+        elif grow.any():
             r_g, j_g = rids[grow], j[grow]
             ids = self._alloc_blocks(int(grow.sum()))
             self.gtab[r_g, j_g] = ids
