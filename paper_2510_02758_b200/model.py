@@ -29,6 +29,15 @@ from . import _lib
 from ._lib import check, lib
 
 _DEBUG_GRAPHS = os.environ.get("TF_DEBUG_GRAPHS") == "1"  # sync + range-check every graph replay (debug)
+# Prompt prefills replayed from the token-bucket graphs (TF_PROMPT_GRAPHS=1)
+# or launched eagerly (default).  The graphs cut the host time of a prompt
+# prefill from ~10 ms to ~0.7 ms, but the reference policy then measures
+# prompt prefills at their true GPU speed, prices recompute accordingly
+# (t_recompute = prefill_s_per_token x ctx) and recomputes 3-6x more often:
+# on the whole C2 burst that churn costs 6-10% effective throughput and
+# +20-30% P99 TTFT (profiles/r2_full_run_prompt_graphs_ab.json).  Recompute
+# prefills always replay graphs (as in round 1).
+_PROMPT_GRAPHS = os.environ.get("TF_PROMPT_GRAPHS", "0") == "1"
 
 
 class _Staging:
@@ -311,7 +320,7 @@ class PagedDecoder:
                                               "use the synthetic KV source for that baseline")
                 else:
                     seqs.append((rid, prompt[lo: hi - 1], lo))
-            if job.kind != "recompute" and self._prefill_fits_graph(seqs) and self.attn_timing is None:
+            if job.kind != "recompute" and _PROMPT_GRAPHS and self._prefill_fits_graph(seqs) and self.attn_timing is None:
                 t0 = self._prefill_graph(dp, seqs, st)
             else:
                 t0 = self._prefill_batch(dp, seqs, st)
