@@ -833,21 +833,31 @@ __global__ void __launch_bounds__(kSelThreads) tick_kernel(TickArgs a) {
   }
 }
 
+// Order-preserving pacing filter (scheduler.py:811-823): keep member i iff
+// b_rem[i] <= rates[i] * lim.  The inputs are read ONCE (coalesced; they may
+// live in mapped host memory) into shared memory, then warp 0 compacts the
+// kept ids in order with ballots.
 __global__ void iteration_kernel(const int32_t* ids, const long long* brem, const double* rates, int n, double lim,
                                  int32_t* out, int32_t* n_out) {
-  // order-preserving filter: rank among kept by prefix count
-  __shared__ int total;
-  if (threadIdx.x == 0) total = 0;
-  __syncthreads();
+  __shared__ uint8_t keep_sh[kMaxN];
+  __shared__ int32_t id_sh[kMaxN];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    if (!((double)brem[i] <= __dmul_rn(rates[i], lim))) continue;
-    int r = 0;
-    for (int j = 0; j < i; ++j) r += ((double)brem[j] <= __dmul_rn(rates[j], lim)) ? 1 : 0;
-    out[r] = ids[i];
-    atomicAdd(&total, 1);
+    keep_sh[i] = ((double)brem[i] <= __dmul_rn(rates[i], lim)) ? 1 : 0;
+    id_sh[i] = ids[i];
   }
   __syncthreads();
-  if (threadIdx.x == 0) *n_out = total;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int base = 0;
+    for (int c = 0; c < n; c += 32) {
+      const int i = c + lane;
+      const bool k = i < n && keep_sh[i];
+      const unsigned bal = __ballot_sync(0xffffffffu, k);
+      if (k) out[base + __popc(bal & ((1u << lane) - 1))] = id_sh[i];
+      base += __popc(bal);
+    }
+    if (lane == 0) *n_out = base;
+  }
 }
 
 __global__ void __launch_bounds__(kSelThreads) select_kernel(const tf_prio* v, int n, double gpu_mem, int max_batch,
@@ -879,6 +889,7 @@ struct Selector {
   char* host;
   int64_t host_bytes;
   int32_t max_n, max_w;
+  char* host_dev;  // device-visible alias of the pinned host workspace (zero-copy I/O)
 };
 
 static std::vector<Selector*> g_sel;
@@ -1110,7 +1121,14 @@ int tf_selector_init(void* dev_ws, int64_t dev_bytes, void* host_pinned_ws, int6
     TF_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)));
     attr_set = true;
   }
-  Selector* S = new Selector{(char*)dev_ws, dev_bytes, (char*)host_pinned_ws, host_bytes, max_members, max_waiting};
+  void* hdev = nullptr;
+  if (cudaHostGetDevicePointer(&hdev, host_pinned_ws, 0) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("tf_selector_init: the host workspace is not pinned / mapped host memory");
+    return TF_EINVAL;
+  }
+  Selector* S = new Selector{(char*)dev_ws, dev_bytes, (char*)host_pinned_ws, host_bytes, max_members, max_waiting,
+                             (char*)hdev};
   g_sel.push_back(S);
   *out_handle = (int64_t)g_sel.size();
   return TF_OK;
@@ -1160,19 +1178,21 @@ int tf_iteration_batch(int64_t sel, const int32_t* ids, const int64_t* b_rem, co
   }
   Layout L = layout(S->max_n, S->max_w);
   cudaStream_t st = (cudaStream_t)stream;
+  // Zero-copy: the kernel reads the (ids, b_rem, rates) rows straight out of
+  // the pinned host workspace and writes its result back there - this call
+  // sits between every decode step's completion and the next dispatch, and
+  // three copy-engine transfers (each a DMA setup, possibly queued behind KV
+  // swaps) cost several times the kernel itself
   char* h = S->host + L.members;
-  char* d = S->dev + L.members;
+  char* hd = S->host_dev + L.members;
   memcpy(h, ids, (size_t)n * 4);
   memcpy(h + 4 * S->max_n, b_rem, (size_t)n * 8);
   memcpy(h + 12 * S->max_n, rates, (size_t)n * 8);
-  TF_CUDA(cudaMemcpyAsync(d, h, (size_t)20 * S->max_n, cudaMemcpyHostToDevice, st));
-  int32_t* dout = (int32_t*)(S->dev + L.preempt);
-  int32_t* dn = (int32_t*)(S->dev + L.counts);
-  iteration_kernel<<<1, 256, 0, st>>>((const int32_t*)d, (const long long*)(d + 4 * S->max_n),
-                                      (const double*)(d + 12 * S->max_n), n, pacing_buffer_seconds, dout, dn);
+  int32_t* dout = (int32_t*)(S->host_dev + L.preempt);
+  int32_t* dn = (int32_t*)(S->host_dev + L.counts);
+  iteration_kernel<<<1, 256, 0, st>>>((const int32_t*)hd, (const long long*)(hd + 4 * S->max_n),
+                                      (const double*)(hd + 12 * S->max_n), n, pacing_buffer_seconds, dout, dn);
   TF_LAUNCH_CHECK();
-  TF_CUDA(cudaMemcpyAsync(S->host + L.counts, dn, 4, cudaMemcpyDeviceToHost, st));
-  TF_CUDA(cudaMemcpyAsync(S->host + L.preempt, dout, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
   TF_CUDA(cudaStreamSynchronize(st));
   *n_out = *(int32_t*)(S->host + L.counts);
   memcpy(out_ids, S->host + L.preempt, (size_t)(*n_out) * 4);
