@@ -66,6 +66,42 @@ class RealtimeEngine(Engine):
         self.skipped_s = 0.0
         self.wall_s = 0.0
         self._stop = False
+        self._defer_wt, self._wt_deferred = False, None
+
+    # ------------------------------------------ write-through after dispatch
+    # The reference plans the next write-through chunks and then dispatches the
+    # next GPU job at the same instant (engine.py _on_decode_iter_done /
+    # _on_prefill_done).  Nothing in the dispatch depends on the plan (d2h
+    # chunks change no HBM accounting), so in real time the dispatch goes
+    # first: the host work of planning and starting a copy (a selector call
+    # and a d2h launch, ~0.1 ms) no longer sits between a decode step's end
+    # and the next step's launch.
+    def _on_decode_iter_done(self, time, subject, batch, iter_time):
+        self._defer_wt = True
+        try:
+            super()._on_decode_iter_done(time, subject, batch, iter_time)
+        finally:
+            self._defer_wt = False
+        self._flush_deferred_wt()
+
+    def _on_prefill_done(self, time, subject, job, duration):
+        self._defer_wt = True
+        try:
+            super()._on_prefill_done(time, subject, job, duration)
+        finally:
+            self._defer_wt = False
+        self._flush_deferred_wt()
+
+    def _plan_write_through(self, time):
+        if self._defer_wt:
+            self._wt_deferred = time
+            return
+        super()._plan_write_through(time)
+
+    def _flush_deferred_wt(self):
+        if self._wt_deferred is not None:
+            t, self._wt_deferred = self._wt_deferred, None
+            super()._plan_write_through(t)
 
     # ------------------------------------------------- fused write-through
     def _after_decode_commit(self, produced):
