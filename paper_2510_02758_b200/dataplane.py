@@ -160,6 +160,9 @@ class GpuDataPlane:
         ws = max(1, int(lib.tf_paged_decode_attn_workspace(pool.handle, max(1, len(reqs)), self.max_len, 64)))
         self._attn_ws = torch.zeros(ws, dtype=torch.uint8, device=dev)
         self.attn_out = None
+        # the tables / workspace above were filled on the default stream; the
+        # compute / copy streams are non-blocking, so order them explicitly
+        torch.cuda.synchronize(dev)
 
     def enable_fused_write_through(self):
         """Mirror every decoded token to the host inside the decode step

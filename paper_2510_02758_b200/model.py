@@ -134,6 +134,10 @@ class PagedDecoder:
         self._pgraphs = {}  # recompute prefill graphs per token bucket
         self._graph_launches = {}  # this library's kernels captured per graph
         self.replayed_launches = 0  # ... and re-run by graph replays so far
+        if self.device.type == "cuda":
+            # weights and buffers were generated on the default stream; every
+            # later use is on the data plane's non-blocking streams
+            torch.cuda.synchronize(self.device)
 
     def launch_count(self) -> int:
         """This library's kernel launches so far: direct C-ABI launches plus
@@ -479,6 +483,11 @@ class PagedDecoder:
             stage = torch.zeros((3, Bp), dtype=torch.int64, pin_memory=True)
             ws_n = max(1, int(lib.tf_paged_decode_attn_workspace(dp.pool.handle, Bp, self._gmax_ctx, self.hq)))
             ws = torch.zeros(ws_n, dtype=torch.uint8, device=self.device)
+            # io / ws were initialised on the default stream and st is a
+            # non-blocking stream: without this the warm-up can read them
+            # before the fills ran (garbage token ids / rows -> an illegal
+            # address, seen with two processes time-slicing one GPU)
+            st.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(st):
                 self._forward_graphable(dp, io, Bp, ws, st)  # warm-up (kernel attributes, cuBLAS handles)
             st.synchronize()
@@ -528,6 +537,7 @@ class PagedDecoder:
             meta[T:2 * T] = torch.arange(T, dtype=torch.int32, device=self.device)
             meta[2 * T + NS + 1] = T  # all real slots empty, padding = [0, T)
             rows, pos32, cu = meta[:T], meta[T:2 * T], meta[2 * T:]
+            st.wait_stream(torch.cuda.current_stream())  # the fills above ran on the default stream
             with torch.cuda.stream(st):
                 self._prefill_core(dp, tok, rows, pos32, cu, T, last, st)  # warm-up
             st.synchronize()
