@@ -171,6 +171,7 @@ class GpuDataPlane:
             raise ValueError("fused write-through changes the token-count semantics; realtime mode only")
         self.fused_wt = True
         self.htable = torch.full_like(self.table, -1)
+        torch.cuda.synchronize(self.pool.device)  # filled on the default stream, read on s_compute
 
     def enable_scratch(self):
         """Reserve one block for the padding rows of captured decode graphs."""

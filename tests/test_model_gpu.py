@@ -89,6 +89,7 @@ def test_decode_step_matches_fp32_reference(cuda, hd):
     for L in model.layers:
         L["ln1"].copy_((1 + 0.2 * torch.randn(shape.hidden, device=cuda)).to(torch.bfloat16))
         L["ln2"].copy_((1 + 0.2 * torch.randn(shape.hidden, device=cuda)).to(torch.bfloat16))
+    torch.cuda.synchronize()  # default-stream writes before the compute stream reads them
     st = dp.s_compute
     with torch.cuda.stream(st):
         first = model._prefill_batch(dp, seqs, st)

@@ -96,6 +96,7 @@ def test_graph_decode_matches_eager(cuda):
     st.synchronize()
     kv_graph = pool.gpu.clone()
     pool.gpu.copy_(snap)
+    torch.cuda.synchronize()  # default-stream restore before the compute stream reads the pool
     with torch.cuda.stream(st):
         toks = torch.tensor([100 + r for r in rids], device=cuda)
         e_out = model._decode_rows(dp, rids, toks, pos, st)

@@ -49,6 +49,7 @@ def _setup(cuda, shape, tp, n_req, nlb):
     dp = GpuDataPlane(reqs, pool, mode="realtime", kv_source="model", model=model,
                       n_q_heads=shape.n_q_heads // size)
     dp.table[:n_req, :nlb] = torch.arange(n_req * nlb, dtype=torch.int32, device=cuda).view(n_req, nlb)
+    torch.cuda.synchronize()  # default-stream setup before the data plane's non-blocking streams
     return model, dp, pool
 
 
@@ -187,6 +188,7 @@ def test_recompute_prefill_graph_matches_eager(cuda):
         sb = dp.scratch_block
         free = [b for b in range(pool.n_blocks) if b != sb]
         dp.table[:2, :nlb] = torch.tensor(free[: 2 * nlb], dtype=torch.int32, device=cuda).view(2, nlb)
+        torch.cuda.synchronize()  # default-stream setup before the compute stream
         toks = torch.randint(0, shape.vocab, (77,), generator=torch.Generator().manual_seed(3))
         st = dp.s_compute
         if use_graph:
@@ -234,6 +236,7 @@ def test_prompt_prefill_graph_matches_eager(cuda):
         dp.enable_scratch()
         free = [b for b in range(pool.n_blocks) if b != dp.scratch_block]
         dp.table[:n_req, :nlb] = torch.tensor(free[: n_req * nlb], dtype=torch.int32, device=cuda).view(n_req, nlb)
+        torch.cuda.synchronize()  # default-stream setup before the compute stream
         st = dp.s_compute
         if use_graph:
             model.enable_graphs(dp, buckets=(8,), prefill_buckets=32)
