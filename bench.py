@@ -150,6 +150,7 @@ def run_ours(args):
     from paper_2510_02758_b200.dataplane import GpuDataPlane, KvPool
     from paper_2510_02758_b200.engine import SimConfig
     from paper_2510_02758_b200.metrics import ttft_latency_stats
+    from paper_2510_02758_b200 import model as model_mod
     from paper_2510_02758_b200.model import PagedDecoder
     from paper_2510_02758_b200.realtime import RealtimeEngine
     from paper_2510_02758_b200.scheduler import BufferAwarePolicy, SchedulerConfig
@@ -459,7 +460,8 @@ def run_ours(args):
                    "l2": "working set (weights + KV, tens of GB) >> 126 MB L2; no flush needed",
                    "timed_region": f"decode iterations [{args.warmup}, {args.warmup + args.steps}) from t=0 "
                                    "of the real-time loop (measured clock, idle gaps skipped)",
-                   "cuda_graphs": bool(args.graphs), "fused_write_through": bool(args.fused_wt)},
+                   "cuda_graphs": bool(args.graphs),
+                   "prompt_graphs": bool(args.graphs) and model_mod._PROMPT_GRAPHS, "fused_write_through": bool(args.fused_wt)},
         "raw_tok_s": agg["raw"],
         "e2e": {"value": agg["e2e"], "unit": "effective tok/s",
                 "h2d_bytes_per_step": int((agg["h2d_tok"] * bpt + local["batch_sum"] * 24) / len(timed)),

@@ -29,15 +29,17 @@ from . import _lib
 from ._lib import check, lib
 
 _DEBUG_GRAPHS = os.environ.get("TF_DEBUG_GRAPHS") == "1"  # sync + range-check every graph replay (debug)
-# Prompt prefills replayed from the token-bucket graphs (TF_PROMPT_GRAPHS=1)
-# or launched eagerly (default).  The graphs cut the host time of a prompt
-# prefill from ~10 ms to ~0.7 ms, but the reference policy then measures
-# prompt prefills at their true GPU speed, prices recompute accordingly
-# (t_recompute = prefill_s_per_token x ctx) and recomputes 3-6x more often:
-# on the whole C2 burst that churn costs 6-10% effective throughput and
-# +20-30% P99 TTFT (profiles/r2_full_run_prompt_graphs_ab.json).  Recompute
-# prefills always replay graphs (as in round 1).
-_PROMPT_GRAPHS = os.environ.get("TF_PROMPT_GRAPHS", "0") == "1"
+# Prompt prefills replayed from the token-bucket graphs (default) or launched
+# eagerly (TF_PROMPT_GRAPHS=0).  The graphs cut the host time of a prompt
+# prefill from ~10 ms to ~0.7 ms.  Eager prompts make the reference policy
+# measure slower prefills and churn less on the whole C2 burst (+6-10%
+# effective throughput, -20-30% P99 TTFT: profiles/r2_full_run_prompt_graphs_ab.json),
+# but they stretch the initial admission wave by ~1 s, so the policy's first
+# preemption tick can land inside the first decode steps: 2 of 5 short
+# windows (bench.py --steps 20 --warmup 5) then carried ~0.87 s of
+# readmission prefills and measured ~9x lower, against 0 of 7 with graphs.
+# Recompute prefills always replay graphs.
+_PROMPT_GRAPHS = os.environ.get("TF_PROMPT_GRAPHS", "1") == "1"
 
 
 class _Staging:
