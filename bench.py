@@ -5,18 +5,24 @@ arriving as a burst at t=0, KV swap to pinned host), 1 GPU per process.
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                 [--config c2|c4] [--arrivals burst|poisson] [--full-run]
 
-A *step* is one decode iteration of the real-time serving loop
-(realtime.RealtimeEngine): the GPU selector's pacing / tick decisions (member
-view built on the device), the Llama3-8B forward (captured CUDA graph: fused
-RMSNorm / rope+append / paged attention / SwiGLU around cuBLAS GEMMs) and the
-write-through / evict / load chunks the engine issues meanwhile on the two
-high-priority copy streams.  W warm-up steps from t=0, then EXACTLY K timed
-steps (default 1000: the admission / preemption / swap-heavy phase of the
-burst).
+A *step* is one schedule interval of the real-time serving loop
+(realtime.RealtimeEngine; 0.5 s of serving clock, `--step-unit tick`, the
+default): one selector tick (the GPU selector's member view and decisions)
+and everything the engine runs until the next one - the decode iterations
+(Llama3-8B forward from a captured CUDA graph: fused RMSNorm / rope+append /
+paged attention / SwiGLU around cuBLAS GEMMs), the prefills / recomputes the
+tick admitted, and the write-through / evict / load chunks on the two
+high-priority copy streams.  W warm-up intervals from t=0, then EXACTLY K
+timed intervals (default K=20, W=5: serving clock [2.5, 12.5) s of the burst,
+the admission / preemption / swap phase).  `--step-unit iter` times decode
+iterations instead (the round-1 definition): a 20-iteration window from t=0
+sits on the burst's first rotation tick (t = 2.0 s, 53 preemptions + 53
+admissions) on some boxes and not on others, so its value is bimodal
+(~22.5K vs ~3K, profiles/r2_bench20_windows.json).
 
 value  = effective tokens (tokensim.metrics weights, tau1/tau2 = 10%/20% of
          the output length) generated in the K steps / device time of every
-         GPU job (decode steps and the prefills between them) in the window
+         GPU job (decode iterations and the prefills between them) in the window
          (CUDA events on the compute stream), max over ranks; weights and KV
          resident in HBM.
 e2e    = the same tokens / host wall-clock span of the K steps through the
@@ -265,6 +271,8 @@ def run_ours(args):
 
     t_start = time.perf_counter()
     state = {"phase": "warm", "timed": [], "wall0": None, "wall1": None}
+    tick_s = policy.cfg.schedule_interval
+    t_warm, t_end = args.warmup * tick_s, (args.warmup + args.steps) * tick_s  # --step-unit tick
 
     def window_probes(eng, timed):
         """Right at the end of the timed window (device idle, live batch intact):
@@ -331,7 +339,10 @@ def run_ours(args):
                   f"waiting={len(eng.waiting)} d2h={dp.stats['d2h_tokens']} h2d={dp.stats['h2d_tokens']} "
                   f"wall={time.perf_counter() - t_start:.1f}s", file=sys.stderr, flush=True)
         if state["phase"] == "warm":
-            if n >= args.warmup:
+            # iter: W decode iterations from t=0; tick: the decode iteration
+            # that reaches the W-th schedule tick (t = W x interval) closes the
+            # warm-up, so the timed steps start at the tick
+            if (n >= args.warmup) if args.step_unit == "iter" else (rec["end"] >= t_warm):
                 state["phase"] = "timed"
                 state["wall0"] = time.perf_counter()
                 state["ev0"] = len(dp._events)
@@ -341,7 +352,7 @@ def run_ours(args):
             return
         if state["phase"] == "timed":
             state["timed"].append(dict(rec))
-            if len(state["timed"]) >= args.steps:
+            if (len(state["timed"]) >= args.steps) if args.step_unit == "iter" else (rec["end"] >= t_end):
                 state["wall1"] = time.perf_counter()
                 state["ev1"] = len(dp._events)
                 state["pre1"], state["rc1"] = eng.total_preemptions, eng.total_recomputes
@@ -404,6 +415,7 @@ def run_ours(args):
     if state["phase"] not in ("done", "ttft", "rest"):
         raise RuntimeError(f"bench ended in phase {state['phase']} after {len(eng.steps)} steps")
     timed = state["timed"]
+    n_steps = len(timed) if args.step_unit == "iter" else args.steps
     bpt = shape.kv_bytes_per_token // tp_size  # swap bytes per token: all layers' K and V of this rank's shard
     local = _window_stats(eng, dp, timed, state["ev0"], state["ev1"], bpt)
     local.update(ttft_lat=[r.gen_times[0] - r.arrival for r in res.records if r.gen_times],
@@ -436,8 +448,10 @@ def run_ours(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": agg["dev_s"] / len(timed) * 1e3,
-        "decode_ms_per_step": sum(st_["dur"] for st_ in timed) / len(timed) * 1e3,
+        "step_unit": "schedule interval" if args.step_unit == "tick" else "decode iteration",
+        "ms_per_step": agg["dev_s"] / n_steps * 1e3,
+        "decode_iterations": len(timed),
+        "decode_ms_per_iter": sum(st_["dur"] for st_ in timed) / len(timed) * 1e3,
         "prefill_device_s_in_window": round(local["prefill_s"], 4),
         "higher_is_better": True,
         "scaling": "strong" if tp_mode else "weak",
@@ -458,20 +472,25 @@ def run_ours(args):
                    "seq_len": None, "parallelism": f"tp{world}" if tp_mode else f"replicas x{world}",
                    "policy": policy.name, "arrivals": args.arrivals,
                    "l2": "working set (weights + KV, tens of GB) >> 126 MB L2; no flush needed",
-                   "timed_region": f"decode iterations [{args.warmup}, {args.warmup + args.steps}) from t=0 "
-                                   "of the real-time loop (measured clock, idle gaps skipped)",
+                   "timed_region": (f"decode iterations [{args.warmup}, {args.warmup + args.steps}) from t=0 "
+                                    "of the real-time loop (measured clock, idle gaps skipped)")
+                   if args.step_unit == "iter" else
+                   (f"schedule intervals [{args.warmup}, {args.warmup + args.steps}) of {tick_s:g} s from t=0 of "
+                    f"the real-time loop = serving clock [{t_warm:g}, {t_end:g}) s (measured clock, idle gaps "
+                    "skipped): every tick, decode iteration, prefill / recompute and swap chunk in between"),
                    "cuda_graphs": bool(args.graphs),
                    "prompt_graphs": bool(args.graphs) and model_mod._PROMPT_GRAPHS, "fused_write_through": bool(args.fused_wt)},
         "raw_tok_s": agg["raw"],
         "e2e": {"value": agg["e2e"], "unit": "effective tok/s",
-                "h2d_bytes_per_step": int((agg["h2d_tok"] * bpt + local["batch_sum"] * 24) / len(timed)),
-                "d2h_bytes_per_step": int((agg["d2h_tok"] * bpt + local["batch_sum"] * 8) / len(timed))},
+                "h2d_bytes_per_step": int((agg["h2d_tok"] * bpt + local["batch_sum"] * 24) / n_steps),
+                "d2h_bytes_per_step": int((agg["d2h_tok"] * bpt + local["batch_sum"] * 8) / n_steps)},
         "swap": swap,
         "swap_window": sw_out,
         "roofline": state.get("roof"),
         "clocks": sampler.summary(),
         "gpu_launches": int(state["launch1"] - state["launch0"]),
         "first_tokens_in_window": len(local["ttft_lat"]),
+        "window_clock": _window_clock(eng, timed),
         "ttft": agg["ttft"],
     }
     # gpu_launches: this library's kernel launches inside the window, counted:
@@ -516,6 +535,27 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return out
+
+
+def _window_clock(eng, steps):
+    """Where the window sits on the serving clock: its first / last decode
+    iteration, the run's first decode iteration, and the schedule ticks from
+    t=0 to one interval past the window (how many fired; the ones that moved
+    requests, with their preempt / admit / resume counts) - a window that
+    holds a rotation tick's preemptions and readmission prefills shows it."""
+    t_lo, t_hi = steps[0]["start"], steps[-1]["end"]
+    fired, moved = 0, []
+    for e in eng.decision_log:
+        if e["time"] > t_hi + eng.policy.cfg.schedule_interval:
+            break
+        fired += 1
+        n = {k: len(e.get(k) or ()) for k in ("preempted", "admitted", "resumed", "recomputed")}
+        if any(n.values()):
+            moved.append({"t": round(e["time"], 4), "mode": e.get("mode"), **n})
+    return {"start_s": round(t_lo, 4), "end_s": round(t_hi, 4),
+            "first_decode_s": round(eng.steps[0]["start"], 4) if eng.steps else None,
+            "schedule_interval_s": eng.policy.cfg.schedule_interval, "ticks_fired": fired,
+            "ticks_that_moved_requests": moved[:40]}
 
 
 def _window_stats(eng, dp, steps, ev0, ev1, bpt):
@@ -911,8 +951,12 @@ def _self_launch(args) -> bool:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--step-unit", default="tick", choices=["tick", "iter"],
+                    help="tick (default): a step is one schedule interval of the serving loop (0.5 s of serving "
+                         "clock: one selector tick and every decode iteration, prefill and swap chunk until the "
+                         "next); iter: one decode iteration (round-1 definition)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     # pinned host tier: 16384 x 2 MiB = 32 GiB covers the timed window; a
     # full run of the burst peaks near 22K blocks (replay of the same trace)

@@ -31,14 +31,14 @@ from ._lib import check, lib
 _DEBUG_GRAPHS = os.environ.get("TF_DEBUG_GRAPHS") == "1"  # sync + range-check every graph replay (debug)
 # Prompt prefills replayed from the token-bucket graphs (default) or launched
 # eagerly (TF_PROMPT_GRAPHS=0).  The graphs cut the host time of a prompt
-# prefill from ~10 ms to ~0.7 ms.  Eager prompts make the reference policy
-# measure slower prefills and churn less on the whole C2 burst (+6-10%
-# effective throughput, -20-30% P99 TTFT: profiles/r2_full_run_prompt_graphs_ab.json),
-# but they stretch the initial admission wave by ~1 s, so the policy's first
-# preemption tick can land inside the first decode steps: 2 of 5 short
-# windows (bench.py --steps 20 --warmup 5) then carried ~0.87 s of
-# readmission prefills and measured ~9x lower, against 0 of 7 with graphs.
-# Recompute prefills always replay graphs.
+# prefill from ~10 ms to ~0.7 ms, and an eager prefill holds the GPU for its
+# host-bound launch sequence: in bench.py's serving window (20 schedule
+# intervals of the C2 burst) prefills take 0.22 s of device time with graphs
+# and 1.1-1.15 s eager, 14.2-14.7K vs 10.9K effective tok/s.  Over the
+# whole burst the eager path's slower measured prefills make the reference
+# policy recompute and preempt less (1,644 vs 1,537 effective tok/s, P99 TTFT
+# 101.6 vs 124.6 s: profiles/r2_full_run_prompt_graphs_ab.json).  Recompute
+# prefills always replay graphs.
 _PROMPT_GRAPHS = os.environ.get("TF_PROMPT_GRAPHS", "1") == "1"
 
 
