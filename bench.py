@@ -886,8 +886,9 @@ def run_reference(args):
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "impl": "reference",
            "config": {"workload": "C2: Llama3-8B bf16 random-init, 256-request burst (the same population and "
                                   "metric as the ours arm); the reference's CPU path = the oracle restatement of one "
-                                  f"decode step at B={args.ref_batch} (the burst's opening decode batch = the ours "
-                                  "arm's window batch from t=0) on the host cores (tokensim itself has no tensors)",
+                                  f"decode step at B={args.ref_batch} (the median decode batch of the ours arm's "
+                                  "default window, 20 schedule intervals of the burst) on the host cores (tokensim "
+                                  "itself has no tensors)",
                       "model": "llama3-8b", "parallelism": "host CPU", "global_batch": args.ref_batch},
            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
                                        "d2h_bytes_per_step": 0}}
@@ -979,8 +980,8 @@ def main():
     ap.add_argument("--max-wall", type=float, default=600.0, help="--full-run: stop (truncated) after this many "
                     "seconds of wall time")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-batch", type=int, default=128, help="reference arm: the decode batch of the timed "
-                    "window (the C2 burst runs at max_batch=128 from t=0)")
+    ap.add_argument("--ref-batch", type=int, default=80, help="reference arm: the decode batch of the timed "
+                    "window (median 78-81 over the default 20 schedule intervals of the C2 burst)")
     ap.add_argument("--policy", default="tokenflow", choices=["tokenflow", "fcfs"], help="fcfs: the paper's "
                     "comparison baseline (tokensim/scheduler.py:828-880) on the same B200 data plane")
     ap.add_argument("--swap-steps", type=int, default=200, help="swap-phase sub-window: decode steps after the first "
