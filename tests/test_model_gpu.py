@@ -9,7 +9,8 @@ within 2e-2 of the row's max |logit| (the north star's bf16 tolerance), and
 the K/V the step appended within bf16 rounding of the reference at layer 0
 and within the same 2e-2 tolerance deeper (bf16 residual stream).
 Covers head_dim 64 (the C1 tiny decoder, bulk-copy attention) and head_dim
-128 (the tensor-core attention the C2 models use)."""
+128 (the tensor-core attention the C2 models use), at 5 rows and at a
+72-row batch."""
 import dataclasses
 import math
 
@@ -73,17 +74,18 @@ def _reference_decode(model, dp, rids, toks, positions):
     return _rms(x, model.ln_f, s.rms_eps) @ model.lm_head.float(), new_kv
 
 
-@pytest.mark.parametrize("hd", [64, 128])
-def test_decode_step_matches_fp32_reference(cuda, hd):
+@pytest.mark.parametrize("hd,n_req", [(64, 6), (128, 6), (128, 72)])
+def test_decode_step_matches_fp32_reference(cuda, hd, n_req):
     from test_tp_gpu import _setup
 
     from paper_2510_02758_b200 import configs
 
     shape = configs.TINY if hd == 64 else dataclasses.replace(
         configs.TINY, name="mini-hd128", hidden=512, n_q_heads=8, n_kv_heads=2, head_dim=128, ffn=1024)
-    n_req, nlb = 6, 8
-    g = torch.Generator().manual_seed(hd)
-    seqs = [(i, torch.randint(0, shape.vocab, (20 + 17 * i,), generator=g), 0) for i in range(n_req)]
+    nlb = 8
+    g = torch.Generator().manual_seed(hd + n_req)
+    seqs = [(i, torch.randint(0, shape.vocab, ((20 + 17 * i) if n_req <= 6 else (20 + 5 * (i % 7)),), generator=g), 0)
+            for i in range(n_req)]
     model, dp, pool = _setup(cuda, shape, None, n_req, nlb)
     # non-trivial norm weights (the synthetic model's are ones)
     for L in model.layers:
@@ -94,7 +96,7 @@ def test_decode_step_matches_fp32_reference(cuda, hd):
     with torch.cuda.stream(st):
         first = model._prefill_batch(dp, seqs, st)
     torch.cuda.synchronize()
-    rids = [0, 2, 3, 5, 1]  # a subset, out of order
+    rids = [0, 2, 3, 5, 1] if n_req <= 6 else list(range(n_req))[::-1]  # out of order
     positions = [seqs[r][1].numel() for r in rids]
     toks = first[rids].to(torch.long)
     ref_logits, ref_kv = _reference_decode(model, dp, rids, toks, positions)

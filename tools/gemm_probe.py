@@ -40,6 +40,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/gemm_probe.json")
     ap.add_argument("--blas", default="default", choices=["default", "cublas", "cublaslt"])
+    ap.add_argument("--ms", default="32,64,96,128", help="comma list of GEMM row counts (decode batch buckets)")
     args = ap.parse_args()
     if args.blas != "default":
         torch.backends.cuda.preferred_blas_library(args.blas)
@@ -47,7 +48,7 @@ def main():
     bf = torch.bfloat16
     rows = []
     # Llama3-8B: wqkv 4096x6144, wo 4096x4096, wgu 4096x28672, wd 14336x4096
-    for M in (32, 64, 96, 128):
+    for M in (int(m) for m in args.ms.split(",")):
         for name, K, N in (("wqkv", 4096, 6144), ("wo", 4096, 4096), ("wgu", 4096, 28672), ("wd", 14336, 4096)):
             # distinct weight copies so consecutive launches do not hit L2
             ws = [torch.randn(K, N, device=dev, dtype=bf) * 0.02 for _ in range(4)]
